@@ -1,0 +1,146 @@
+"""Best-fit offset planning on the GPU — drop-in for ``memplan.solve_bestfit``.
+
+The reference heuristic (bestfit.py:276-309, paper §3.2) runs as the
+sm_100a planner kernels in ``csrc/plan.cu`` behind the C ABI
+``mp_plan_bestfit`` / ``mp_plan_bestfit_batched``.  Results are bit-exact
+with the reference: same offsets per block id, same peak.
+
+There is no CPU path: without the built library or a CUDA device these
+functions raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .core import DsaInstance, MemplanError, Plan, Provenance
+
+
+class IllegalLift(MemplanError):
+    """lift_up on the only offset line (reference bestfit.py:34-35)."""
+
+
+class ContainmentViolation(MemplanError):
+    """A block placed on a line that does not contain its lifetime
+    (reference bestfit.py:38-39)."""
+
+
+class NoDevice(MemplanError):
+    """No CUDA device: the planner has no CPU fallback."""
+
+
+def check(rc: int) -> None:
+    """Raise the reference exception class that matches a C-ABI status."""
+    if rc == N.MP_OK:
+        return
+    msg = N.last_error()
+    from . import arena as A
+    from .core import DoubleFree, UnbalancedResume
+    table = {
+        N.MP_ERR_INVALID: ValueError,
+        N.MP_ERR_ILLEGAL_LIFT: IllegalLift,
+        N.MP_ERR_NO_DEVICE: NoDevice,
+        N.MP_ERR_DOUBLE_FREE: DoubleFree,
+        N.MP_ERR_UNKNOWN_ID: A.UnknownId,
+        N.MP_ERR_EXTRA_REQUEST: A.ExtraRequest,
+        N.MP_ERR_ALLOC_AFTER_CLOSE: A.AllocAfterClose,
+        N.MP_ERR_LIVE_AT_RESET: A.LiveBlocksAtReset,
+        N.MP_ERR_UNBALANCED_RESUME: UnbalancedResume,
+        N.MP_ERR_INVALID_PLAN: A.InvalidPlan,
+        N.MP_ERR_OUT_OF_MEMORY: A.OutOfMemory,
+        N.MP_ERR_NEGATIVE_SIZE: ValueError,
+    }
+    if rc == N.MP_ERR_LOOP_BOUND:
+        raise AssertionError(msg or "best-fit loop exceeded its iteration bound")
+    exc = table.get(rc)
+    if exc is None:
+        raise RuntimeError(f"memplan_b200 CUDA failure: {msg}")
+    raise exc(msg)
+
+
+def plan_info() -> dict:
+    """Diagnostics of the last plan call on this thread (steps, lifts, ...)."""
+    info = N.PlanInfo()
+    N.lib().mp_plan_last_info(ctypes.byref(info))
+    return {name: getattr(info, name) for name, _ in N.PlanInfo._fields_}
+
+
+def solve_bestfit_arrays(alloc, free, size, *, device: int = 0, stream: int = 0,
+                         flags: int = 0) -> tuple[np.ndarray, int]:
+    """Array fast path: int64 columns in id order -> (offsets[n], peak).
+
+    Inputs must already satisfy the DsaInstance invariants (sizes >= 1 and
+    aligned, 0 <= alloc < free); they are trusted like the reference's
+    solver trusts its instance."""
+    a, f, s = N.as_i64(alloc), N.as_i64(free), N.as_i64(size)
+    n = len(a)
+    if not (len(f) == n and len(s) == n):
+        raise ValueError("alloc, free and size must have equal length")
+    off = np.empty(n, dtype=np.int64)
+    peak = np.zeros(1, dtype=np.int64)
+    rc = N.lib().mp_plan_bestfit(N.ptr(a), N.ptr(f), N.ptr(s), n, N.ptr(off), N.ptr(peak),
+                                 flags, device, stream or None)
+    check(rc)
+    return off, int(peak[0])
+
+
+def solve_bestfit_device(alloc_d, free_d, size_d, offsets_d, peak_d, n: int, *,
+                         device: int = 0, stream: int = 0, flags: int = 0) -> None:
+    """Device-pointer path: all five arguments are device addresses (ints)
+    of int64 buffers already resident in HBM."""
+    rc = N.lib().mp_plan_bestfit(alloc_d, free_d, size_d, n, offsets_d, peak_d,
+                                 flags | N.MP_DEVICE_PTRS, device, stream or None)
+    check(rc)
+
+
+def solve_bestfit(instance: DsaInstance) -> Plan:
+    """Pack all blocks with the best-fit skyline heuristic on the GPU.
+
+    Same contract as the reference: deterministic, offsets keyed by block
+    id, peak = max(offset + size), provenance BESTFIT."""
+    n = len(instance.blocks)
+    if n == 0:
+        return Plan(offsets={}, peak=0, provenance=Provenance.BESTFIT)
+    a, f, s = instance.arrays()
+    off, peak = solve_bestfit_arrays(a, f, s)
+    return Plan(offsets=dict(zip(range(1, n + 1), off.tolist())), peak=peak,
+                provenance=Provenance.BESTFIT)
+
+
+def solve_bestfit_batched_arrays(trace_ptr, alloc, free, size, *, device: int = 0,
+                                 stream: int = 0, flags: int = 0):
+    """T independent traces in CSR form -> (offsets CSR-aligned, peaks[T])."""
+    tp = N.as_i64(trace_ptr)
+    a, f, s = N.as_i64(alloc), N.as_i64(free), N.as_i64(size)
+    T = len(tp) - 1
+    off = np.empty(len(a), dtype=np.int64)
+    peaks = np.zeros(max(T, 0), dtype=np.int64)
+    rc = N.lib().mp_plan_bestfit_batched(N.ptr(tp), N.ptr(a), N.ptr(f), N.ptr(s), T,
+                                         N.ptr(off), N.ptr(peaks), flags, device,
+                                         stream or None)
+    check(rc)
+    return off, peaks
+
+
+def solve_bestfit_batched(instances: Sequence[DsaInstance], *, device: int = 0) -> list[Plan]:
+    """Plan many independent instances in one batched launch."""
+    cols = [inst.arrays() for inst in instances]
+    sizes = [len(c[0]) for c in cols]
+    tp = np.zeros(len(cols) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=tp[1:])
+    if tp[-1] == 0:
+        return [Plan({}, 0, Provenance.BESTFIT) for _ in instances]
+    a = np.concatenate([c[0] for c in cols]) if cols else np.zeros(0, np.int64)
+    f = np.concatenate([c[1] for c in cols]) if cols else np.zeros(0, np.int64)
+    s = np.concatenate([c[2] for c in cols]) if cols else np.zeros(0, np.int64)
+    off, peaks = solve_bestfit_batched_arrays(tp, a, f, s, device=device)
+    plans = []
+    for t, n in enumerate(sizes):
+        seg = off[tp[t]:tp[t + 1]].tolist()
+        plans.append(Plan(offsets=dict(zip(range(1, n + 1), seg)), peak=int(peaks[t]),
+                          provenance=Provenance.BESTFIT))
+    return plans

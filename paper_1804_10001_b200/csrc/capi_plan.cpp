@@ -1,0 +1,114 @@
+// extern "C" planning entry points (include/memplan_b200.h).
+#include <string.h>
+
+#include <vector>
+
+#include "common.h"
+#include "plan.h"
+
+using namespace mp;
+
+namespace {
+
+int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *alloc,
+               const int64_t *free_, const int64_t *size, int64_t T, int64_t *offsets_out,
+               int64_t *peaks_out, int flags, int device, cudaStream_t s) {
+    MP_TRY(use_device(device));
+    if (T < 0) {
+        set_error("negative trace count");
+        return MP_ERR_INVALID;
+    }
+    std::vector<int64_t> tp_h((size_t)T + 1);
+    if (trace_ptr_is_dev) {
+        MP_CUDA(cudaMemcpyAsync(tp_h.data(), trace_ptr, sizeof(int64_t) * (T + 1),
+                                cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+    } else {
+        memcpy(tp_h.data(), trace_ptr, sizeof(int64_t) * (T + 1));
+    }
+    for (int64_t t = 0; t < T; t++) {
+        if (tp_h[t + 1] < tp_h[t]) {
+            set_error("trace_ptr must be non-decreasing");
+            return MP_ERR_INVALID;
+        }
+    }
+    const int64_t N = T ? tp_h[T] : 0;
+    if (flags & MP_DEVICE_PTRS) {
+        const int64_t *tp_d = trace_ptr;
+        Scratch tps;
+        if (!trace_ptr_is_dev) {
+            MP_TRY(tps.alloc(sizeof(int64_t) * (T + 1), s));
+            MP_CUDA(cudaMemcpyAsync(tps.ptr, tp_h.data(), sizeof(int64_t) * (T + 1),
+                                    cudaMemcpyHostToDevice, s));
+            tp_d = tps.as<int64_t>();
+        }
+        return plan_device(tp_d, tp_h.data(), T, alloc, free_, size, offsets_out, peaks_out,
+                           flags, device, s);
+    }
+    // host pointers: stage through one device buffer
+    const size_t nb = sizeof(int64_t) * (size_t)N;
+    Scratch buf;
+    MP_TRY(buf.alloc(4 * nb + sizeof(int64_t) * (2 * T + 1) + 5 * 256, s));
+    Carver cv(buf.ptr, buf.bytes);
+    int64_t *a_d = cv.take<int64_t>(N), *f_d = cv.take<int64_t>(N), *s_d = cv.take<int64_t>(N);
+    int64_t *o_d = cv.take<int64_t>(N), *p_d = cv.take<int64_t>(T), *tp_d = cv.take<int64_t>(T + 1);
+    MP_CUDA(cudaMemcpyAsync(tp_d, tp_h.data(), sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, s));
+    if (N) {
+        MP_CUDA(cudaMemcpyAsync(a_d, alloc, nb, cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaMemcpyAsync(f_d, free_, nb, cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaMemcpyAsync(s_d, size, nb, cudaMemcpyHostToDevice, s));
+    }
+    MP_TRY(plan_device(tp_d, tp_h.data(), T, a_d, f_d, s_d, o_d, p_d, flags, device, s));
+    if (N) MP_CUDA(cudaMemcpyAsync(offsets_out, o_d, nb, cudaMemcpyDeviceToHost, s));
+    if (T) MP_CUDA(cudaMemcpyAsync(peaks_out, p_d, sizeof(int64_t) * T, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    return MP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mp_plan_bestfit(const int64_t *alloc, const int64_t *free_, const int64_t *size, int64_t n,
+                    int64_t *offsets_out, int64_t *peak_out, int flags, int device,
+                    mp_stream_t stream) {
+    if (n < 0) {
+        set_error("negative block count");
+        return MP_ERR_INVALID;
+    }
+    int64_t tp[2] = {0, n};
+    if (flags & MP_DEVICE_PTRS) {
+        // peak_out is a device pointer too
+        return plan_entry(tp, false, alloc, free_, size, 1, offsets_out, peak_out, flags, device,
+                          (cudaStream_t)stream);
+    }
+    return plan_entry(tp, false, alloc, free_, size, 1, offsets_out, peak_out, flags, device,
+                      (cudaStream_t)stream);
+}
+
+int mp_plan_bestfit_batched(const int64_t *trace_ptr, const int64_t *alloc, const int64_t *free_,
+                            const int64_t *size, int64_t T, int64_t *offsets_out,
+                            int64_t *peaks_out, int flags, int device, mp_stream_t stream) {
+    return plan_entry(trace_ptr, (flags & MP_DEVICE_PTRS) != 0, alloc, free_, size, T, offsets_out,
+                      peaks_out, flags, device, (cudaStream_t)stream);
+}
+
+int mp_plan_last_info(mp_plan_info *out) {
+    *out = last_plan_info();
+    return MP_OK;
+}
+
+const char *mp_last_error(void) { return last_error(); }
+
+int mp_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+const char *mp_version(void) { return "memplan_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

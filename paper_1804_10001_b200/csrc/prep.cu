@@ -1,0 +1,324 @@
+// K0 — planner pre-pass on the device: compressed time ranks, (alloc, id)
+// order, priority ranks, and the packed tables K1/K2 read.
+//
+// Replaces _RemainingBlocks.__init__ (bestfit.py:231-241: sort by
+// (alloc, id), int64 columns) and the implicit key of take_best
+// (bestfit.py:250-256: lifetime, then size, then smaller id).
+//
+// Batched form: T traces in CSR (trace_ptr).  Every sort is a stable CUB
+// radix sort; the per-trace grouping is restored by a final stable sort on
+// the trace index (LSD order), so a single pass handles one or many traces.
+#include <cub/cub.cuh>
+
+#include "common.h"
+#include "plan_types.cuh"
+#include "prep.h"
+
+namespace mp {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t n) {
+    int64_t g = (n + kThreads - 1) / kThreads;
+    return (int)(g < 1 ? 1 : (g > (1 << 30) ? (1 << 30) : g));
+}
+
+__global__ void k_trace_index(const int64_t *__restrict__ trace_ptr, int64_t T,
+                              uint32_t *__restrict__ tix, int64_t N) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = T;  // last t with trace_ptr[t] <= i
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (trace_ptr[mid] <= i) lo = mid; else hi = mid;
+        }
+        tix[i] = (uint32_t)lo;
+    }
+}
+
+// times[0..N) = alloc, times[N..2N) = free; idx = iota
+__global__ void k_fill_times(const int64_t *__restrict__ alloc, const int64_t *__restrict__ free_,
+                             int64_t N, int64_t *__restrict__ times, uint32_t *__restrict__ idx) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        times[i] = i < N ? alloc[i] : free_[i - N];
+        idx[i] = (uint32_t)i;
+    }
+}
+
+__global__ void k_gather_tkey(const uint32_t *__restrict__ idx, const uint32_t *__restrict__ tix,
+                              int64_t N, int64_t M, uint32_t *__restrict__ tkey) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = idx[i];
+        tkey[i] = tix[v < N ? v : v - N];
+    }
+}
+
+// flag = 1 where a new (trace, time) group starts in sorted order
+__global__ void k_rank_flags(const uint32_t *__restrict__ idx, const int64_t *__restrict__ alloc,
+                             const int64_t *__restrict__ free_, const uint32_t *__restrict__ tix,
+                             int64_t N, uint32_t *__restrict__ flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = idx[i];
+        int64_t tv = v < N ? alloc[v] : free_[v - N];
+        uint32_t tt = tix[v < N ? v : v - N];
+        uint32_t f = 1;
+        if (i > 0) {
+            uint32_t u = idx[i - 1];
+            int64_t tu = u < N ? alloc[u] : free_[u - N];
+            uint32_t tu_t = tix[u < N ? u : u - N];
+            f = (tu != tv || tu_t != tt) ? 1u : 0u;
+        }
+        flags[i] = f;
+    }
+}
+
+// local rank = inclusive scan - scan at the trace's first sorted element
+__global__ void k_rank_scatter(const uint32_t *__restrict__ idx, const uint32_t *__restrict__ scan,
+                               const uint32_t *__restrict__ tix,
+                               const int64_t *__restrict__ trace_ptr, int64_t N,
+                               uint32_t *__restrict__ arank, uint32_t *__restrict__ frank) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = idx[i];
+        int64_t k = v < N ? v : v - N;
+        uint32_t t = tix[k];
+        uint32_t r = scan[i] - scan[2 * trace_ptr[t]];
+        if (v < N) arank[k] = r; else frank[k] = r;
+    }
+}
+
+__global__ void k_trace_U(const uint32_t *__restrict__ scan, const int64_t *__restrict__ trace_ptr,
+                          int64_t T, uint32_t *__restrict__ U) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t a = trace_ptr[t], b = trace_ptr[t + 1];
+        U[t] = b > a ? scan[2 * b - 1] - scan[2 * a] + 1 : 0;
+    }
+}
+
+__global__ void k_iota_keys_arank(const uint32_t *__restrict__ arank, int64_t N,
+                                  uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = arank[i];
+        vals[i] = (uint32_t)i;
+    }
+}
+
+// descending size / lifetime as ascending complemented unsigned keys
+__global__ void k_keys_size(const int64_t *__restrict__ size, int64_t N,
+                            uint64_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = ~(uint64_t)size[i];
+        vals[i] = (uint32_t)i;
+    }
+}
+
+__global__ void k_keys_life(const uint32_t *__restrict__ vals, const int64_t *__restrict__ alloc,
+                            const int64_t *__restrict__ free_, int64_t N,
+                            uint64_t *__restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t k = vals[i];
+        keys[i] = ~(uint64_t)(free_[k] - alloc[k]);
+    }
+}
+
+__global__ void k_gather_tix32(const uint32_t *__restrict__ vals, const uint32_t *__restrict__ tix,
+                               int64_t N, uint32_t *__restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = tix[vals[i]];
+}
+
+// order[p] = k for global position p; write pos/prio inverse maps
+__global__ void k_inverse(const uint32_t *__restrict__ order, const uint32_t *__restrict__ tix,
+                          const int64_t *__restrict__ trace_ptr, int64_t N,
+                          uint32_t *__restrict__ inv) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t k = order[p];
+        inv[k] = (uint32_t)(p - trace_ptr[tix[k]]);
+    }
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *v, uint32_t n, uint32_t x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (v[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// sorted alloc ranks per position, for the apos/fpos binary searches
+__global__ void k_sorted_arank(const uint32_t *__restrict__ order, const uint32_t *__restrict__ arank,
+                               int64_t N, uint32_t *__restrict__ sar) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N;
+         p += (int64_t)gridDim.x * blockDim.x)
+        sar[p] = arank[order[p]];
+}
+
+__global__ void k_pack(const uint32_t *__restrict__ tix, const int64_t *__restrict__ trace_ptr,
+                       const uint32_t *__restrict__ arank, const uint32_t *__restrict__ frank,
+                       const uint32_t *__restrict__ posof, const uint32_t *__restrict__ prio,
+                       const uint32_t *__restrict__ sar, const int64_t *__restrict__ size,
+                       int64_t N, uint2 *__restrict__ ent, Rec *__restrict__ rec) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t t = tix[k];
+        int64_t b = trace_ptr[t];
+        uint32_t n = (uint32_t)(trace_ptr[t + 1] - b);
+        const uint32_t *s = sar + b;
+        Rec r;
+        r.pos = posof[k];
+        r.arank = arank[k];
+        r.frank = frank[k];
+        r.apos = lower_bound_u32(s, n, r.arank);
+        r.fpos = lower_bound_u32(s, n, r.frank);
+        r.k = (uint32_t)(k - b);
+        r.size = size[k];
+        rec[b + prio[k]] = r;
+        ent[b + r.pos] = make_uint2(r.frank, prio[k]);
+    }
+}
+
+inline int bits_for(int64_t T) {
+    int b = 1;
+    while ((int64_t(1) << b) < T) b++;
+    return b;
+}
+
+}  // namespace
+
+size_t prep_scratch_bytes(int64_t N, int64_t T) {
+    size_t M = (size_t)2 * N;
+    size_t b = 0;
+    b += Carver::need<uint32_t>(N);         // tix
+    b += Carver::need<int64_t>(M) * 2;      // times in/out
+    b += Carver::need<uint32_t>(M) * 2;     // idx in/out
+    b += Carver::need<uint32_t>(M) * 2;     // tkeys / flags+scan (reused)
+    b += Carver::need<uint32_t>(N) * 6;     // arank frank posof prio sar order
+    b += Carver::need<uint64_t>(N) * 2;     // 64-bit keys in/out
+    // CUB temp: radix sort of M pairs + scan of M items
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, (const int64_t *)nullptr, (int64_t *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)M);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)M);
+    cub::DeviceScan::InclusiveSum(nullptr, t3, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (int)M);
+    size_t tmax = t1 > t2 ? t1 : t2;
+    tmax = tmax > t3 ? tmax : t3;
+    b += Carver::need<char>(tmax);
+    b += Carver::need<uint32_t>(T);  // U
+    return b + 4096;
+}
+
+int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes,
+             cudaStream_t s) {
+    const int64_t N = in.N, T = in.T, M = 2 * N;
+    if (N == 0) {
+        if (T > 0) MP_CUDA(cudaMemsetAsync(out.U, 0, sizeof(uint32_t) * T, s));
+        return MP_OK;
+    }
+    if (M >= (int64_t(1) << 31)) {
+        set_error("batch too large for 32-bit ranks");
+        return MP_ERR_INVALID;
+    }
+    Carver cv(scratch, scratch_bytes);
+    uint32_t *tix = cv.take<uint32_t>(N);
+    int64_t *times = cv.take<int64_t>(M), *times_s = cv.take<int64_t>(M);
+    uint32_t *idx = cv.take<uint32_t>(M), *idx_s = cv.take<uint32_t>(M);
+    uint32_t *tk = cv.take<uint32_t>(M), *tk_s = cv.take<uint32_t>(M);
+    uint32_t *arank = cv.take<uint32_t>(N), *frank = cv.take<uint32_t>(N);
+    uint32_t *posof = cv.take<uint32_t>(N), *prio = cv.take<uint32_t>(N);
+    uint32_t *sar = cv.take<uint32_t>(N), *order = cv.take<uint32_t>(N);
+    uint64_t *k64 = cv.take<uint64_t>(N), *k64_s = cv.take<uint64_t>(N);
+    size_t tbytes = 0;
+    {
+        size_t t1 = 0, t2 = 0, t3 = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, t1, (const int64_t *)nullptr, (int64_t *)nullptr,
+                                        (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)M);
+        cub::DeviceRadixSort::SortPairs(nullptr, t2, (const uint64_t *)nullptr,
+                                        (uint64_t *)nullptr, (const uint32_t *)nullptr,
+                                        (uint32_t *)nullptr, (int)M);
+        cub::DeviceScan::InclusiveSum(nullptr, t3, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                      (int)M);
+        tbytes = t1 > t2 ? t1 : t2;
+        tbytes = tbytes > t3 ? tbytes : t3;
+    }
+    void *tmp = cv.take<char>(tbytes);
+    if (cv.off > cv.cap) {
+        set_error("prep scratch too small");
+        return MP_ERR_CUDA;
+    }
+    const int tb = bits_for(T);
+    const int g1 = grid_for(N), g2 = grid_for(M);
+
+    k_trace_index<<<g1, kThreads, 0, s>>>(in.trace_ptr, T, tix, N);
+
+    // ---- compressed time ranks over alloc ∪ free, per trace ----
+    k_fill_times<<<g2, kThreads, 0, s>>>(in.alloc, in.free_, N, times, idx);
+    size_t tb_ = tbytes;
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, times, times_s, idx, idx_s, (int)M, 0, 64, s));
+    uint32_t *rk_idx = idx_s;
+    if (T > 1) {
+        k_gather_tkey<<<g2, kThreads, 0, s>>>(idx_s, tix, N, M, tk);
+        tb_ = tbytes;
+        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, tk, tk_s, idx_s, idx, (int)M, 0, tb, s));
+        rk_idx = idx;
+    }
+    uint32_t *flags = tk, *scan = tk_s;
+    k_rank_flags<<<g2, kThreads, 0, s>>>(rk_idx, in.alloc, in.free_, tix, N, flags);
+    tb_ = tbytes;
+    MP_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb_, flags, scan, (int)M, s));
+    k_rank_scatter<<<g2, kThreads, 0, s>>>(rk_idx, scan, tix, in.trace_ptr, N, arank, frank);
+    k_trace_U<<<grid_for(T), kThreads, 0, s>>>(scan, in.trace_ptr, T, out.U);
+
+    // ---- (alloc, id) order: stable by alloc rank, then stable by trace ----
+    uint32_t *ka = tk, *ka_s = tk_s, *va = idx, *va_s = idx_s;
+    k_iota_keys_arank<<<g1, kThreads, 0, s>>>(arank, N, ka, va);
+    tb_ = tbytes;
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, ka, ka_s, va, va_s, (int)N, 0, 32, s));
+    uint32_t *ord = va_s;
+    if (T > 1) {
+        k_gather_tix32<<<g1, kThreads, 0, s>>>(va_s, tix, N, ka);
+        tb_ = tbytes;
+        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, ka, ka_s, va_s, va, (int)N, 0, tb, s));
+        ord = va;
+    }
+    MP_CUDA(cudaMemcpyAsync(order, ord, sizeof(uint32_t) * N, cudaMemcpyDeviceToDevice, s));
+    k_inverse<<<g1, kThreads, 0, s>>>(order, tix, in.trace_ptr, N, posof);
+    k_sorted_arank<<<g1, kThreads, 0, s>>>(order, arank, N, sar);
+
+    // ---- priority order: stable size desc, then stable lifetime desc, then trace ----
+    uint32_t *vp = idx, *vp_s = idx_s;
+    k_keys_size<<<g1, kThreads, 0, s>>>(in.size, N, k64, vp);
+    tb_ = tbytes;
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, k64, k64_s, vp, vp_s, (int)N, 0, 64, s));
+    k_keys_life<<<g1, kThreads, 0, s>>>(vp_s, in.alloc, in.free_, N, k64);
+    tb_ = tbytes;
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, k64, k64_s, vp_s, vp, (int)N, 0, 64, s));
+    uint32_t *pord = vp;
+    if (T > 1) {
+        k_gather_tix32<<<g1, kThreads, 0, s>>>(vp, tix, N, tk);
+        tb_ = tbytes;
+        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, tk, tk_s, vp, vp_s, (int)N, 0, tb, s));
+        pord = vp_s;
+    }
+    k_inverse<<<g1, kThreads, 0, s>>>(pord, tix, in.trace_ptr, N, prio);
+
+    k_pack<<<g1, kThreads, 0, s>>>(tix, in.trace_ptr, arank, frank, posof, prio, sar, in.size, N,
+                                   out.ent, out.rec);
+    MP_CUDA(cudaGetLastError());
+    return MP_OK;
+}
+
+}  // namespace mp

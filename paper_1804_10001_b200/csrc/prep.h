@@ -1,0 +1,26 @@
+// K0 interface (see prep.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "plan_types.cuh"
+
+namespace mp {
+
+struct PrepIn {
+    const int64_t *trace_ptr;  // device, T+1
+    const int64_t *alloc, *free_, *size;  // device, N each
+    int64_t N, T;
+};
+
+struct PrepOut {
+    uint2 *ent;   // device, N (alloc order per trace)
+    Rec *rec;     // device, N (priority order per trace)
+    uint32_t *U;  // device, T (time-rank count per trace)
+};
+
+size_t prep_scratch_bytes(int64_t N, int64_t T);
+int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes,
+             cudaStream_t s);
+
+}  // namespace mp

@@ -1,0 +1,57 @@
+"""GPU planner parity against the reference golden vectors and the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import blocks_arrays
+
+pytestmark = pytest.mark.gpu
+
+
+def test_small_golden(small_plans):
+    from paper_1804_10001_b200.bestfit import solve_bestfit_arrays
+    for case in small_plans:
+        a, f, s = blocks_arrays(case["blocks"])
+        off, peak = solve_bestfit_arrays(a, f, s)
+        assert peak == case["peak"], case["name"]
+        assert off.tolist() == case["offsets"], case["name"]
+
+
+@pytest.mark.parametrize("name", ["cnn_1e4", "uniform_1e4", "walk_1e4"])
+def test_large_golden(large_plans, name):
+    from paper_1804_10001_b200.bestfit import solve_bestfit_arrays, plan_info
+    b = large_plans[name + "_blocks"]
+    for flags in (0, 4):
+        off, peak = solve_bestfit_arrays(b[:, 1], b[:, 2], b[:, 0], flags=flags)
+        assert peak == int(large_plans[name + "_peak"][0])
+        assert np.array_equal(off, large_plans[name + "_offsets"])
+        print(name, flags, plan_info())
+
+
+def test_batched_golden(small_plans):
+    from paper_1804_10001_b200.bestfit import solve_bestfit_batched_arrays
+    cases = small_plans
+    sizes = [len(c["blocks"]) for c in cases]
+    tp = np.zeros(len(cases) + 1, np.int64)
+    np.cumsum(sizes, out=tp[1:])
+    cols = [blocks_arrays(c["blocks"]) for c in cases]
+    a = np.concatenate([c[0] for c in cols]); f = np.concatenate([c[1] for c in cols])
+    s = np.concatenate([c[2] for c in cols])
+    off, peaks = solve_bestfit_batched_arrays(tp, a, f, s)
+    for t, c in enumerate(cases):
+        assert peaks[t] == c["peak"], c["name"]
+        assert off[tp[t]:tp[t + 1]].tolist() == c["offsets"], c["name"]
+
+
+def test_random_vs_oracle():
+    from paper_1804_10001_b200.bestfit import solve_bestfit_arrays
+    rng = np.random.default_rng(0)
+    for trial in range(60):
+        n = int(rng.integers(1, 3000))
+        T = int(rng.integers(2, 4 * n + 3))
+        a = rng.integers(0, T - 1, n)
+        f = a + 1 + (rng.integers(0, T, n) % (T - a))
+        s = rng.integers(1, 1 << int(rng.integers(1, 40)), n)
+        off, peak = solve_bestfit_arrays(a, f, s)
+        ooff, opeak = oracle.solve_bestfit(a, f, s)
+        assert peak == opeak and np.array_equal(off, ooff), trial
