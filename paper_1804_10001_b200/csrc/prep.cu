@@ -165,10 +165,66 @@ __global__ void k_sorted_arank(const uint32_t *__restrict__ order, const uint32_
         sar[p] = arank[order[p]];
 }
 
+__device__ __forceinline__ int64_t gcd64(int64_t a, int64_t b) {
+    while (b) {
+        int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+// Per-trace size unit g = gcd(sizes) and total bytes in units (saturating).
+// Every skyline height is a sum of sizes, hence a multiple of g; when the
+// total is below 2^32 units the planner runs on 32-bit heights and packs
+// (height, lo) into one 64-bit argmin key.
+__global__ void k_trace_scale(const int64_t *__restrict__ trace_ptr,
+                              const int64_t *__restrict__ size, int64_t *__restrict__ unit,
+                              uint64_t *__restrict__ total_units) {
+    __shared__ int64_t sg[32];
+    __shared__ uint64_t ss[32];
+    const int64_t t = blockIdx.x;
+    const int64_t b = trace_ptr[t], e = trace_ptr[t + 1];
+    int64_t g = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) g = gcd64(size[i], g);
+    for (int o = 16; o; o >>= 1) g = gcd64(g, __shfl_xor_sync(0xFFFFFFFFu, g, o));
+    if ((threadIdx.x & 31) == 0) sg[threadIdx.x >> 5] = g;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        g = threadIdx.x < (blockDim.x >> 5) ? sg[threadIdx.x] : 0;
+        for (int o = 16; o; o >>= 1) g = gcd64(g, __shfl_xor_sync(0xFFFFFFFFu, g, o));
+        if (threadIdx.x == 0) sg[0] = g > 0 ? g : 1;
+    }
+    __syncthreads();
+    g = sg[0];
+    const uint64_t cap = uint64_t(1) << 62;
+    uint64_t acc = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        acc += (uint64_t)(size[i] / g);
+        if (acc > cap) acc = cap;
+    }
+    for (int o = 16; o; o >>= 1) {
+        acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+        if (acc > cap) acc = cap;
+    }
+    if ((threadIdx.x & 31) == 0) ss[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            tot += ss[w];
+            if (tot > cap) tot = cap;
+        }
+        unit[t] = g;
+        total_units[t] = tot;
+    }
+}
+
 __global__ void k_pack(const uint32_t *__restrict__ tix, const int64_t *__restrict__ trace_ptr,
                        const uint32_t *__restrict__ arank, const uint32_t *__restrict__ frank,
                        const uint32_t *__restrict__ posof, const uint32_t *__restrict__ prio,
                        const uint32_t *__restrict__ sar, const int64_t *__restrict__ size,
+                       const int64_t *__restrict__ unit,
                        int64_t N, uint2 *__restrict__ ent, Rec *__restrict__ rec) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
          k += (int64_t)gridDim.x * blockDim.x) {
@@ -183,7 +239,7 @@ __global__ void k_pack(const uint32_t *__restrict__ tix, const int64_t *__restri
         r.apos = lower_bound_u32(s, n, r.arank);
         r.fpos = lower_bound_u32(s, n, r.frank);
         r.k = (uint32_t)(k - b);
-        r.size = size[k];
+        r.size = size[k] / unit[t];  // in units of the trace's size gcd
         rec[b + prio[k]] = r;
         ent[b + r.pos] = make_uint2(r.frank, prio[k]);
     }
@@ -225,7 +281,10 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
              cudaStream_t s) {
     const int64_t N = in.N, T = in.T, M = 2 * N;
     if (N == 0) {
-        if (T > 0) MP_CUDA(cudaMemsetAsync(out.U, 0, sizeof(uint32_t) * T, s));
+        if (T > 0) {
+            MP_CUDA(cudaMemsetAsync(out.U, 0, sizeof(uint32_t) * T, s));
+            MP_CUDA(cudaMemsetAsync(out.total_units, 0, sizeof(uint64_t) * T, s));
+        }
         return MP_OK;
     }
     if (M >= (int64_t(1) << 31)) {
@@ -315,8 +374,10 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
     }
     k_inverse<<<g1, kThreads, 0, s>>>(pord, tix, in.trace_ptr, N, prio);
 
-    k_pack<<<g1, kThreads, 0, s>>>(tix, in.trace_ptr, arank, frank, posof, prio, sar, in.size, N,
-                                   out.ent, out.rec);
+    k_trace_scale<<<(unsigned)T, kThreads, 0, s>>>(in.trace_ptr, in.size, out.unit,
+                                                  out.total_units);
+    k_pack<<<g1, kThreads, 0, s>>>(tix, in.trace_ptr, arank, frank, posof, prio, sar, in.size,
+                                   out.unit, N, out.ent, out.rec);
     MP_CUDA(cudaGetLastError());
     return MP_OK;
 }

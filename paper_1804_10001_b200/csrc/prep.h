@@ -17,6 +17,8 @@ struct PrepOut {
     uint2 *ent;   // device, N (alloc order per trace)
     Rec *rec;     // device, N (priority order per trace)
     uint32_t *U;  // device, T (time-rank count per trace)
+    int64_t *unit;         // device, T: gcd of the trace's sizes
+    uint64_t *total_units; // device, T: sum(size)/unit, saturating at 2^62
 };
 
 size_t prep_scratch_bytes(int64_t N, int64_t T);

@@ -55,3 +55,30 @@ def test_random_vs_oracle():
         off, peak = solve_bestfit_arrays(a, f, s)
         ooff, opeak = oracle.solve_bestfit(a, f, s)
         assert peak == opeak and np.array_equal(off, ooff), trial
+
+
+def test_line_overflow_restart():
+    """A staircase of 3000 disjoint blocks needs 5999 skyline lines, more than
+    the shared-memory line capacity: the planner must restart it with global
+    line storage and still match the oracle."""
+    from paper_1804_10001_b200.bestfit import solve_bestfit_arrays, plan_info
+    k = np.arange(3000, dtype=np.int64)
+    a, f, s = 2 * k, 2 * k + 1, k + 1
+    off, peak = solve_bestfit_arrays(a, f, s)
+    ooff, opeak = oracle.solve_bestfit(a, f, s)
+    assert peak == opeak == 3000 and np.array_equal(off, ooff)
+    assert plan_info()["engine"] & 32  # restarted with global lines
+
+
+def test_wide_heights_64bit():
+    """Total bytes above 2^32 units select the 64-bit height engine."""
+    from paper_1804_10001_b200.bestfit import solve_bestfit_arrays, plan_info
+    rng = np.random.default_rng(5)
+    n = 500
+    a = rng.integers(0, 900, n)
+    f = a + 1 + rng.integers(0, 100, n)
+    s = rng.integers(1, 1 << 40, n) * 3 + 1
+    off, peak = solve_bestfit_arrays(a, f, s)
+    ooff, opeak = oracle.solve_bestfit(a, f, s)
+    assert peak == opeak and np.array_equal(off, ooff)
+    assert not (plan_info()["engine"] & 16)
