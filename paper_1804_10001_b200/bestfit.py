@@ -103,8 +103,6 @@ def solve_bestfit(instance: DsaInstance) -> Plan:
     Same contract as the reference: deterministic, offsets keyed by block
     id, peak = max(offset + size), provenance BESTFIT."""
     n = len(instance.blocks)
-    if n == 0:
-        return Plan(offsets={}, peak=0, provenance=Provenance.BESTFIT)
     a, f, s = instance.arrays()
     off, peak = solve_bestfit_arrays(a, f, s)
     return Plan(offsets=dict(zip(range(1, n + 1), off.tolist())), peak=peak,
@@ -132,8 +130,6 @@ def solve_bestfit_batched(instances: Sequence[DsaInstance], *, device: int = 0) 
     sizes = [len(c[0]) for c in cols]
     tp = np.zeros(len(cols) + 1, dtype=np.int64)
     np.cumsum(sizes, out=tp[1:])
-    if tp[-1] == 0:
-        return [Plan({}, 0, Provenance.BESTFIT) for _ in instances]
     a = np.concatenate([c[0] for c in cols]) if cols else np.zeros(0, np.int64)
     f = np.concatenate([c[1] for c in cols]) if cols else np.zeros(0, np.int64)
     s = np.concatenate([c[2] for c in cols]) if cols else np.zeros(0, np.int64)
