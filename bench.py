@@ -1,0 +1,363 @@
+"""Benchmark: best-fit planning throughput on B200 (blocks planned / s).
+
+Workload (BASELINE.json configs[4], "synthetic random-lifetime traces, 10^4-
+10^6 blocks ... vs host-CPU reference"): every GPU plans a batch of
+--traces synthetic uniform-random-lifetime traces of --n blocks each
+(alloc ~ U[0,2n), free ~ U(alloc, 2n], size ~ U[1, 2^20] rounded to 512 B),
+seeded per rank -> weak scaling.  One step = one batched plan of the
+rank's traces (+ the rank-0 gather when N > 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Inputs total > L2 (126 MB) per step, so no L2 flush is needed.  `value` is
+device-timed with inputs resident in HBM; `e2e` goes through the public C ABI
+with pinned host buffers (H2D + D2H inside the timed region).  The
+reference arm times the CPU restatement of the reference (oracle/, numpy,
+same algorithm and vectorisation as memplan.bestfit) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "blocks planned/sec and plan latency (bit-exact peak bytes); replay ns/alloc"
+UNIT = "blocks/s"
+ALIGN = 512
+
+
+def make_batch(n: int, traces: int, seed: int):
+    """CSR batch of uniform random-lifetime traces (sizes aligned to 512)."""
+    from paper_1804_10001_b200.workloads import uniform_arrays
+    tp = np.arange(traces + 1, dtype=np.int64) * n
+    A = np.empty(n * traces, np.int64)
+    F = np.empty_like(A)
+    S = np.empty_like(A)
+    for t in range(traces):
+        a, f, s = uniform_arrays(n, seed * 100003 + t)
+        sl = slice(t * n, (t + 1) * n)
+        A[sl], F[sl], S[sl] = a, f, ((s + ALIGN - 1) // ALIGN) * ALIGN
+    return tp, A, F, S
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md "clocks DURING the timed region")
+# ---------------------------------------------------------------------------
+class Clocks:
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, name in enumerate(names):
+                if len(r) > 3 + k and r[3 + k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: numpy restatement of memplan.bestfit on the host cores
+# ---------------------------------------------------------------------------
+def _cpu_one(args):
+    n, seed = args
+    from oracle.bestfit_np import solve_bestfit_np
+    tp, A, F, S = make_batch(n, 1, seed)
+    t0 = time.perf_counter()
+    solve_bestfit_np(A, F, S)
+    return time.perf_counter() - t0
+
+
+def cpu_reference(n: int, procs: int, seed: int) -> dict:
+    """Plan `procs` traces, one per process in parallel; blocks/s over the
+    wall time of the batch (the reference is single-threaded per trace)."""
+    import multiprocessing as mpc
+    ctx = mpc.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        t0 = time.perf_counter()
+        per = pool.map(_cpu_one, [(n, seed * 1000 + i) for i in range(procs)])
+        wall = time.perf_counter() - t0
+    return {"value": procs * n / wall, "wall_s": wall, "per_trace_s": statistics.mean(per),
+            "cores": procs}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    procs = min(host_cores(), args.cpu_procs)
+    # warm-up: import numpy/oracle in the workers on a small trace
+    for _ in range(args.warmup):
+        cpu_reference(2000, procs, 99)
+    vals, walls = [], []
+    for k in range(args.steps):
+        r = cpu_reference(args.n, procs, 1 + k)
+        vals.append(r["value"])
+        walls.append(r["wall_s"])
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * float(np.median(walls)), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": bench_config(args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{procs} traces x {args.n} blocks per step, one per "
+                                   f"process (oracle/bestfit_np.py: numpy restatement of "
+                                   f"memplan.bestfit, same algorithm/vectorisation)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_config(args, world):
+    return {"workload": f"uniform random-lifetime traces, n={args.n} blocks each, "
+                        f"{args.traces} traces per GPU per step (BASELINE.json configs[4])",
+            "n_blocks_per_trace": args.n, "traces_per_gpu": args.traces,
+            "global_batch_traces": args.traces * world, "alignment": ALIGN,
+            "parallelism": f"traces sharded over {world} GPU(s), gather to rank 0",
+            "l2": "inputs larger than L2 per step (no flush needed)"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+    import ctypes
+    from paper_1804_10001_b200 import _native as N
+    from paper_1804_10001_b200.bestfit import check, plan_info
+    from paper_1804_10001_b200 import dist as D
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    lib = N.lib()
+
+    tp, A, F, S = make_batch(args.n, args.traces, seed=rank + 1)
+    T, NB = args.traces, len(A)
+    d_tp = torch.from_numpy(tp).to(dev)
+    d_a, d_f, d_s = (torch.from_numpy(x).to(dev) for x in (A, F, S))
+    d_off = torch.empty(NB, dtype=torch.int64, device=dev)
+    d_pk = torch.empty(T, dtype=torch.int64, device=dev)
+
+    def step_device(flags=0):
+        rc = lib.mp_plan_bestfit_batched(d_tp.data_ptr(), d_a.data_ptr(), d_f.data_ptr(),
+                                         d_s.data_ptr(), T, d_off.data_ptr(), d_pk.data_ptr(),
+                                         N.MP_DEVICE_PTRS | flags, local_rank, sh)
+        check(rc)
+
+    # algorithmic bytes: B_alg = 24*sum(W_live) + 32*n per trace
+    step_device(N.MP_STATS)
+    info_stats = plan_info()
+    b_alg = 24 * info_stats["sum_wlive"] + 32 * NB
+
+    # parity spot check (outside the timed region): trace 0 vs the C oracle
+    parity = None
+    if args.check and rank == 0:
+        import oracle
+        off0, pk0 = oracle.solve_bestfit(A[:args.n], F[:args.n], S[:args.n])
+        got = d_off[:args.n].cpu().numpy()
+        parity = bool(np.array_equal(got, off0) and int(d_pk[0]) == pk0)
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+
+    my_ids = list(range(rank * T, rank * T + T))
+    clocks = Clocks(local_rank)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kern_ms, launches = [], 0
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_device()
+        info = plan_info()
+        kern_ms.append(info["kernel_ms"])
+        launches += int(info["launches"])
+        if world > 1:  # the only collective: gather results to rank 0 (NCCL)
+            D.gather_device(my_ids, d_off, d_pk)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * NB / (ms / 1e3)
+
+    # e2e: public C ABI with pinned host buffers (H2D + D2H inside the region)
+    h_tp = torch.from_numpy(tp).pin_memory()
+    h_a, h_f, h_s = (torch.from_numpy(x).pin_memory() for x in (A, F, S))
+    h_off = torch.empty(NB, dtype=torch.int64).pin_memory()
+    h_pk = torch.empty(T, dtype=torch.int64).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        check(lib.mp_plan_bestfit_batched(h_tp.data_ptr(), h_a.data_ptr(), h_f.data_ptr(),
+                                          h_s.data_ptr(), T, h_off.data_ptr(), h_pk.data_ptr(),
+                                          0, local_rank, sh))
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * NB / (e2e_ms / 1e3)
+
+    # single-trace latency (one trace of the same family, device pointers)
+    lat_ms = None
+    if rank == 0:
+        n = args.n
+        o1 = torch.empty(n, dtype=torch.int64, device=dev)
+        p1 = torch.empty(1, dtype=torch.int64, device=dev)
+        for _ in range(2):
+            check(lib.mp_plan_bestfit(d_a.data_ptr(), d_f.data_ptr(), d_s.data_ptr(), n,
+                                      o1.data_ptr(), p1.data_ptr(), N.MP_DEVICE_PTRS,
+                                      local_rank, sh))
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        check(lib.mp_plan_bestfit(d_a.data_ptr(), d_f.data_ptr(), d_s.data_ptr(), n,
+                                  o1.data_ptr(), p1.data_ptr(), N.MP_DEVICE_PTRS, local_rank, sh))
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        lat_ms = e0.elapsed_time(e1)
+        single_info = plan_info()
+
+    if rank == 0:
+        peak, peak_kind = measured_peak()
+        kms = float(np.median(kern_ms))
+        achieved = b_alg / (kms / 1e3) / 1e9
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            procs = min(host_cores(), args.cpu_procs)
+            r = cpu_reference(args.n, procs, 7)
+            cpu = {"value": r["value"], "unit": UNIT, "cores": procs, "kind": "port",
+                   "sample": f"{procs} traces x {args.n} blocks, one per process "
+                             f"({r['per_trace_s']:.1f} s/trace; oracle/bestfit_np.py numpy "
+                             f"restatement of memplan.bestfit)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic", "config": bench_config(args, world),
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(8 * (3 * NB + T + 1)),
+                    "d2h_bytes_per_step": int(8 * (NB + T))},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_kind,
+                         "kernel": "k_plan_sorted (K1 planner)",
+                         "bytes_def": "B_alg = 24*sum(W_live) + 32*n per trace (SURVEY §8(d))",
+                         "alg_bytes_per_launch": b_alg, "kernel_ms": kms},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "single_trace": {"n": args.n, "latency_ms": lat_ms,
+                             "blocks_per_s": args.n / (lat_ms / 1e3) if lat_ms else None,
+                             "steps": single_info["steps"] if lat_ms else None},
+            "plan_info": {k: info_stats[k] for k in ("steps", "lifts", "max_lines", "engine",
+                                                     "sum_wlive")},
+            "parity_trace0_vs_oracle": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=100_000)
+    p.add_argument("--traces", type=int, default=296)
+    p.add_argument("--cpu-procs", type=int, default=32)
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--check", action="store_true", default=True)
+    p.add_argument("--no-check", dest="check", action="store_false")
+    args = p.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

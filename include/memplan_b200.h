@@ -58,7 +58,8 @@ typedef enum {
 enum {
     MP_DEVICE_PTRS = 1 << 0, /* array args are device pointers             */
     MP_ASYNC = 1 << 1,       /* do not synchronise the stream (device ptrs) */
-    MP_FORCE_GLOBAL = 1 << 2 /* debug: keep tables in global memory          */
+    MP_FORCE_GLOBAL = 1 << 2, /* debug: keep tables in global memory         */
+    MP_STATS = 1 << 3         /* count reference window entries (sum_wlive)  */
 };
 
 /* Per-plan diagnostics of the last mp_plan_* call on this thread. */
@@ -67,9 +68,12 @@ typedef struct {
     int64_t lifts;        /* iterations that lifted a line, :300-302        */
     int64_t max_lines;    /* high-water mark of skyline line slots          */
     float prep_ms;        /* K0 (sort/rank/pack) device time                */
-    float plan_ms;        /* K1/K2 planner device time                      */
+    float plan_ms;        /* K1/K2 planner device time incl. status check   */
+    float kernel_ms;      /* first planner launch alone (CUDA events)       */
     int32_t engine;       /* which planner variant ran      */
     int32_t cluster;      /* CTAs per trace                                 */
+    int64_t sum_wlive;    /* with MP_STATS: live window entries, all steps  */
+    int64_t launches;     /* kernels launched by this call                  */
 } mp_plan_info;
 
 /* ---- planning: replaces solve_bestfit(instance) -> Plan (bestfit.py:276) */

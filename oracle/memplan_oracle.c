@@ -199,13 +199,20 @@ int orc_solve_bestfit(int64_t n, const int64_t *alloc, const int64_t *free_,
     s.first = new_line(&s, t_lo, t_hi, 0);
     hpush(&s, s.first); s.nalive = 1;
 
+    /* SoA columns in (alloc, id) order; compacted like bestfit.py:264-273 */
     int64_t *ord = (int64_t *)malloc((size_t)n * sizeof(int64_t));
     for (int64_t k = 0; k < n; k++) ord[k] = k;
     g_alloc_for_sort = alloc;
     qsort(ord, (size_t)n, sizeof(int64_t), cmp_alloc_id);
     int64_t *sa = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t *sf = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t *ss = (int64_t *)malloc((size_t)n * sizeof(int64_t));
     unsigned char *live = (unsigned char *)malloc((size_t)n);
-    for (int64_t i = 0; i < n; i++) { sa[i] = alloc[ord[i]]; live[i] = 1; }
+    for (int64_t i = 0; i < n; i++) {
+        int64_t k = ord[i];
+        sa[i] = alloc[k]; sf[i] = free_[k]; ss[i] = size[k]; live[i] = 1;
+    }
+    int64_t m = n, dead = 0;
 
     int rc = 0;
     int64_t placed = 0, peak = 0;
@@ -217,19 +224,16 @@ int orc_solve_bestfit(int64_t n, const int64_t *alloc, const int64_t *free_,
         int64_t lo = s.ln[line].lo, hi = s.ln[line].hi;
         /* take_best (bestfit.py:243-262): window, fit mask, key max of
          * (lifetime, size, -id) */
-        int64_t i0 = lower_bound(sa, n, lo), i1 = lower_bound(sa, n, hi);
-        int64_t best = -1, bl = 0, bs = 0;
+        int64_t i0 = lower_bound(sa, m, lo), i1 = lower_bound(sa, m, hi);
+        int64_t best = -1, bl = 0, bs = 0, bk = 0;
         for (int64_t i = i0; i < i1; i++) {
             if (!live[i]) continue;
             st->sum_wlive++;
-            int64_t k = ord[i];
-            if (free_[k] > hi) continue;
-            int64_t life = free_[k] - alloc[k];
-            /* ascending id within equal (life,size): first seen wins only if
-             * its id is smaller; ids are not monotone in alloc order */
-            if (best < 0 || life > bl || (life == bl && (size[k] > bs ||
-                (size[k] == bs && k < ord[best])))) {
-                best = i; bl = life; bs = size[k];
+            if (sf[i] > hi) continue;
+            int64_t life = sf[i] - sa[i];
+            if (best < 0 || life > bl || (life == bl && (ss[i] > bs ||
+                (ss[i] == bs && ord[i] < bk)))) {
+                best = i; bl = life; bs = ss[i]; bk = ord[i];
             }
         }
         if (best < 0) {
@@ -238,14 +242,25 @@ int orc_solve_bestfit(int64_t n, const int64_t *alloc, const int64_t *free_,
             continue;
         }
         live[best] = 0;
+        dead++;
         int64_t k = ord[best];
         int64_t off = place(&s, line, alloc[k], free_[k], size[k]);
         offsets_out[k] = off;
         if (off + size[k] > peak) peak = off + size[k];
         placed++;
+        if (dead * 2 > m) {
+            int64_t w = 0;
+            for (int64_t i = 0; i < m; i++) {
+                if (!live[i]) continue;
+                sa[w] = sa[i]; sf[w] = sf[i]; ss[w] = ss[i]; ord[w] = ord[i]; live[w] = 1;
+                w++;
+            }
+            m = w;
+            dead = 0;
+        }
     }
     *peak_out = peak;
-    free(ord); free(sa); free(live); free(s.ln); free(s.hp);
+    free(ord); free(sa); free(sf); free(ss); free(live); free(s.ln); free(s.hp);
     return rc;
 }
 

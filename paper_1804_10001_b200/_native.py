@@ -36,6 +36,7 @@ MP_ERR_NEGATIVE_SIZE = 14
 MP_DEVICE_PTRS = 1
 MP_ASYNC = 2
 MP_FORCE_GLOBAL = 4
+MP_STATS = 8
 
 P64 = ctypes.POINTER(ctypes.c_int64)
 PU64 = ctypes.POINTER(ctypes.c_uint64)
@@ -46,8 +47,9 @@ VP = ctypes.c_void_p
 class PlanInfo(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_int64), ("lifts", ctypes.c_int64),
                 ("max_lines", ctypes.c_int64), ("prep_ms", ctypes.c_float),
-                ("plan_ms", ctypes.c_float), ("engine", ctypes.c_int32),
-                ("cluster", ctypes.c_int32)]
+                ("plan_ms", ctypes.c_float), ("kernel_ms", ctypes.c_float),
+                ("engine", ctypes.c_int32), ("cluster", ctypes.c_int32),
+                ("sum_wlive", ctypes.c_int64), ("launches", ctypes.c_int64)]
 
 
 class VerifyReportC(ctypes.Structure):

@@ -25,8 +25,26 @@ static_assert(sizeof(Rec) == 32, "Rec must stay 32 bytes");
 // rank.  A placed block is overwritten with DEAD so it neither fits nor wins.
 constexpr uint32_t kDead = 0xFFFFFFFFu;
 
+// Chunk-sorted window table (replaces a flat (alloc,id)-ordered table).
+// Positions in (alloc, id) order are grouped into 32-entry chunks; within a
+// chunk the entries are sorted by compressed free rank.  Per slot:
+//   SF = (free_rank << 5) | position-within-chunk   (padding: 0xFFFFFFFF)
+//   SP = priority rank, kDead once placed / padding
+//   PM = inclusive prefix min of SP over the chunk's sorted slots
+// A block fits a line iff free_rank <= hi, i.e. SF <= (hi << 5 | 31), so
+// the fitting entries of a chunk are a prefix and their best priority is
+// PM[count - 1].  Per chunk summary (uint4): min / max live free rank,
+// best live priority (= PM[31]), live count.
+// Chunk index of a trace's chunk j: (trace_base >> 5) + t + j (disjoint per
+// trace for any CSR layout).
+constexpr int kRankBits = 27;  // free ranks must stay below 2^27
+
+__host__ __device__ inline int64_t chunk_base(int64_t trace_base, int64_t t) {
+    return (trace_base >> 5) + t;
+}
+
 // Per-trace planner statistics slots.
-enum { ST_STEPS = 0, ST_LIFTS = 1, ST_MAXLINES = 2, ST_STATUS = 3, ST_N = 4 };
+enum { ST_STEPS = 0, ST_LIFTS = 1, ST_MAXLINES = 2, ST_STATUS = 3, ST_WLIVE = 4, ST_N = 5 };
 
 // Planner status values written to stats[ST_STATUS].
 enum { PS_OK = 0, PS_LOOP_BOUND = 2, PS_ILLEGAL_LIFT = 3, PS_LINES_OVERFLOW = 100 };

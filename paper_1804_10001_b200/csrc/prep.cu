@@ -10,6 +10,8 @@
 // the trace index (LSD order), so a single pass handles one or many traces.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "common.h"
 #include "plan_types.cuh"
 #include "prep.h"
@@ -245,6 +247,63 @@ __global__ void k_pack(const uint32_t *__restrict__ tix, const int64_t *__restri
     }
 }
 
+// One warp per chunk: bitonic-sort the chunk's 32 (free rank, slot) keys,
+// emit SF/SP/PM and the chunk summary.
+__global__ void k_chunk_sort(const int64_t *__restrict__ trace_ptr, int64_t T,
+                             const uint2 *__restrict__ ent, uint32_t *__restrict__ sf,
+                             uint32_t *__restrict__ sp, uint32_t *__restrict__ pm,
+                             uint4 *__restrict__ summ, int64_t nchunks) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t cg = warp; cg < nchunks; cg += nw) {
+        // owning trace: last t with chunk_base(trace_ptr[t], t) <= cg
+        int64_t lo = 0, hi = T;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (chunk_base(trace_ptr[mid], mid) <= cg) lo = mid; else hi = mid;
+        }
+        const int64_t t = lo, b = trace_ptr[t], n = trace_ptr[t + 1] - b;
+        const int64_t j = cg - chunk_base(b, t);
+        if (j >= ((n + 31) >> 5)) continue;  // gap between traces
+        const int64_t p = 32 * j + lane;
+        uint32_t key = 0xFFFFFFFFu, pr = kDead;
+        if (p < n) {
+            const uint2 e = ent[b + p];
+            key = (e.x << 5) | (uint32_t)lane;
+            pr = e.y;
+        }
+        // bitonic sort ascending by key across the warp (payload pr)
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                const uint32_t ok = __shfl_xor_sync(0xFFFFFFFFu, key, jj);
+                const uint32_t op = __shfl_xor_sync(0xFFFFFFFFu, pr, jj);
+                const bool up = ((lane & k) == 0);
+                const bool lower = ((lane & jj) == 0);
+                const bool take = (lower == up) ? ok < key : ok > key;
+                if (take) { key = ok; pr = op; }
+            }
+        }
+        uint32_t m = pr;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, m, o);
+            if (lane >= o) m = min(m, v);
+        }
+        sf[32 * cg + lane] = key;
+        sp[32 * cg + lane] = pr;
+        pm[32 * cg + lane] = m;
+        const unsigned live = __ballot_sync(0xFFFFFFFFu, pr != kDead);
+        const uint32_t fr = key >> 5;
+        const uint32_t mn = live ? __shfl_sync(0xFFFFFFFFu, fr, __ffs(live) - 1) : 0xFFFFFFFFu;
+        const uint32_t mx = live ? __shfl_sync(0xFFFFFFFFu, fr, 31 - __clz(live)) : 0u;
+        const uint32_t bp = __shfl_sync(0xFFFFFFFFu, m, 31);
+        if (lane == 0) summ[cg] = make_uint4(mn, mx, bp, (uint32_t)__popc(live));
+    }
+}
+
 inline int bits_for(int64_t T) {
     int b = 1;
     while ((int64_t(1) << b) < T) b++;
@@ -277,6 +336,9 @@ size_t prep_scratch_bytes(int64_t N, int64_t T) {
     return b + 4096;
 }
 
+thread_local int g_prep_k = 0;
+int prep_launches() { return g_prep_k; }
+
 int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes,
              cudaStream_t s) {
     const int64_t N = in.N, T = in.T, M = 2 * N;
@@ -291,6 +353,7 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
         set_error("batch too large for 32-bit ranks");
         return MP_ERR_INVALID;
     }
+    g_prep_k = 0;
     Carver cv(scratch, scratch_bytes);
     uint32_t *tix = cv.take<uint32_t>(N);
     int64_t *times = cv.take<int64_t>(M), *times_s = cv.take<int64_t>(M);
@@ -322,62 +385,85 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
     const int g1 = grid_for(N), g2 = grid_for(M);
 
     k_trace_index<<<g1, kThreads, 0, s>>>(in.trace_ptr, T, tix, N);
+    g_prep_k++;
 
     // ---- compressed time ranks over alloc ∪ free, per trace ----
     k_fill_times<<<g2, kThreads, 0, s>>>(in.alloc, in.free_, N, times, idx);
+    g_prep_k++;
     size_t tb_ = tbytes;
     MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, times, times_s, idx, idx_s, (int)M, 0, 64, s));
     uint32_t *rk_idx = idx_s;
     if (T > 1) {
         k_gather_tkey<<<g2, kThreads, 0, s>>>(idx_s, tix, N, M, tk);
+        g_prep_k++;
         tb_ = tbytes;
         MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, tk, tk_s, idx_s, idx, (int)M, 0, tb, s));
         rk_idx = idx;
     }
     uint32_t *flags = tk, *scan = tk_s;
     k_rank_flags<<<g2, kThreads, 0, s>>>(rk_idx, in.alloc, in.free_, tix, N, flags);
+    g_prep_k++;
     tb_ = tbytes;
     MP_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb_, flags, scan, (int)M, s));
     k_rank_scatter<<<g2, kThreads, 0, s>>>(rk_idx, scan, tix, in.trace_ptr, N, arank, frank);
+    g_prep_k++;
     k_trace_U<<<grid_for(T), kThreads, 0, s>>>(scan, in.trace_ptr, T, out.U);
+    g_prep_k++;
 
     // ---- (alloc, id) order: stable by alloc rank, then stable by trace ----
     uint32_t *ka = tk, *ka_s = tk_s, *va = idx, *va_s = idx_s;
     k_iota_keys_arank<<<g1, kThreads, 0, s>>>(arank, N, ka, va);
+    g_prep_k++;
     tb_ = tbytes;
     MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, ka, ka_s, va, va_s, (int)N, 0, 32, s));
     uint32_t *ord = va_s;
     if (T > 1) {
         k_gather_tix32<<<g1, kThreads, 0, s>>>(va_s, tix, N, ka);
+        g_prep_k++;
         tb_ = tbytes;
         MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, ka, ka_s, va_s, va, (int)N, 0, tb, s));
         ord = va;
     }
     MP_CUDA(cudaMemcpyAsync(order, ord, sizeof(uint32_t) * N, cudaMemcpyDeviceToDevice, s));
     k_inverse<<<g1, kThreads, 0, s>>>(order, tix, in.trace_ptr, N, posof);
+    g_prep_k++;
     k_sorted_arank<<<g1, kThreads, 0, s>>>(order, arank, N, sar);
+    g_prep_k++;
 
     // ---- priority order: stable size desc, then stable lifetime desc, then trace ----
     uint32_t *vp = idx, *vp_s = idx_s;
     k_keys_size<<<g1, kThreads, 0, s>>>(in.size, N, k64, vp);
+    g_prep_k++;
     tb_ = tbytes;
     MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, k64, k64_s, vp, vp_s, (int)N, 0, 64, s));
     k_keys_life<<<g1, kThreads, 0, s>>>(vp_s, in.alloc, in.free_, N, k64);
+    g_prep_k++;
     tb_ = tbytes;
     MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, k64, k64_s, vp_s, vp, (int)N, 0, 64, s));
     uint32_t *pord = vp;
     if (T > 1) {
         k_gather_tix32<<<g1, kThreads, 0, s>>>(vp, tix, N, tk);
+        g_prep_k++;
         tb_ = tbytes;
         MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, tk, tk_s, vp, vp_s, (int)N, 0, tb, s));
         pord = vp_s;
     }
     k_inverse<<<g1, kThreads, 0, s>>>(pord, tix, in.trace_ptr, N, prio);
+    g_prep_k++;
 
     k_trace_scale<<<(unsigned)T, kThreads, 0, s>>>(in.trace_ptr, in.size, out.unit,
                                                   out.total_units);
+    g_prep_k++;
     k_pack<<<g1, kThreads, 0, s>>>(tix, in.trace_ptr, arank, frank, posof, prio, sar, in.size,
                                    out.unit, N, out.ent, out.rec);
+    g_prep_k++;
+    if (out.sf) {
+        const int64_t chunks = N / 32 + T + 1;
+        const int blocks = (int)std::min<int64_t>((chunks + 7) / 8, 148 * 64);
+        k_chunk_sort<<<blocks, 256, 0, s>>>(in.trace_ptr, T, out.ent, out.sf, out.sp, out.pm,
+                                            out.summ, chunks);
+        g_prep_k++;
+    }
     MP_CUDA(cudaGetLastError());
     return MP_OK;
 }

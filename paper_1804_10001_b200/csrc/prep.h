@@ -14,7 +14,10 @@ struct PrepIn {
 };
 
 struct PrepOut {
-    uint2 *ent;   // device, N (alloc order per trace)
+    uint2 *ent;   // device, N (alloc order per trace): (free rank, priority)
+    // chunk-sorted table, 32 slots per chunk, chunk_base() indexing
+    uint32_t *sf, *sp, *pm;
+    uint4 *summ;  // per chunk
     Rec *rec;     // device, N (priority order per trace)
     uint32_t *U;  // device, T (time-rank count per trace)
     int64_t *unit;         // device, T: gcd of the trace's sizes
@@ -22,6 +25,8 @@ struct PrepOut {
 };
 
 size_t prep_scratch_bytes(int64_t N, int64_t T);
+// kernels (incl. CUB passes) launched by the last prep_run on this thread
+int prep_launches();
 int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes,
              cudaStream_t s);
 

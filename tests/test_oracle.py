@@ -48,3 +48,14 @@ def test_oracle_verify_matches_reference(verify_golden):
         span, pk = t_hi - t_lo, r["peak_recomputed"]
         util = r["used"] / (pk * span) if pk > 0 and span > 0 else 0.0
         assert repr(util) == case["utilization"]
+
+
+def test_numpy_port_matches_reference(small_plans, large_plans):
+    from oracle.bestfit_np import solve_bestfit_np
+    for case in small_plans[:400]:
+        a, f, s = blocks_arrays(case["blocks"])
+        off, peak = solve_bestfit_np(a, f, s)
+        assert peak == case["peak"] and off.tolist() == case["offsets"], case["name"]
+    b = large_plans["walk_1e4_blocks"]
+    off, peak = solve_bestfit_np(b[:, 1], b[:, 2], b[:, 0])
+    assert np.array_equal(off, large_plans["walk_1e4_offsets"])
