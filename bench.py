@@ -2,7 +2,8 @@
 
 Workload (BASELINE.json configs[4], "synthetic random-lifetime traces, 10^4-
 10^6 blocks ... vs host-CPU reference"): every GPU plans a batch of
---traces synthetic uniform-random-lifetime traces of --n blocks each
+--traces (default 1184 = 8 per SM) synthetic uniform-random-lifetime traces
+of --n (default 10^5) blocks each
 (alloc ~ U[0,2n), free ~ U(alloc, 2n], size ~ U[1, 2^20] rounded to 512 B),
 seeded per rank -> weak scaling.  One step = one batched plan of the
 rank's traces (+ the rank-0 gather when N > 1).
@@ -342,7 +343,7 @@ def main():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--n", type=int, default=100_000)
-    p.add_argument("--traces", type=int, default=296)
+    p.add_argument("--traces", type=int, default=1184)
     p.add_argument("--cpu-procs", type=int, default=32)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--check", action="store_true", default=True)

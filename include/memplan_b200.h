@@ -74,6 +74,10 @@ typedef struct {
     int32_t cluster;      /* CTAs per trace                                 */
     int64_t sum_wlive;    /* with MP_STATS: live window entries, all steps  */
     int64_t launches;     /* kernels launched by this call                  */
+    int64_t diag[4];      /* with MP_STATS: choose scans, skeleton passes,
+                             table segments read, edge rows read           */
+    int64_t cycles[4];    /* with env MEMPLAN_TIMING: SM cycles spent in the
+                             choose / query / update / retire phases        */
 } mp_plan_info;
 
 /* ---- planning: replaces solve_bestfit(instance) -> Plan (bestfit.py:276) */

@@ -49,7 +49,8 @@ class PlanInfo(ctypes.Structure):
                 ("max_lines", ctypes.c_int64), ("prep_ms", ctypes.c_float),
                 ("plan_ms", ctypes.c_float), ("kernel_ms", ctypes.c_float),
                 ("engine", ctypes.c_int32), ("cluster", ctypes.c_int32),
-                ("sum_wlive", ctypes.c_int64), ("launches", ctypes.c_int64)]
+                ("sum_wlive", ctypes.c_int64), ("launches", ctypes.c_int64),
+                ("diag", ctypes.c_int64 * 4), ("cycles", ctypes.c_int64 * 4)]
 
 
 class VerifyReportC(ctypes.Structure):

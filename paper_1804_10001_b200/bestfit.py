@@ -66,7 +66,13 @@ def plan_info() -> dict:
     """Diagnostics of the last plan call on this thread (steps, lifts, ...)."""
     info = N.PlanInfo()
     N.lib().mp_plan_last_info(ctypes.byref(info))
-    return {name: getattr(info, name) for name, _ in N.PlanInfo._fields_}
+    out = {name: getattr(info, name) for name, _ in N.PlanInfo._fields_
+           if name not in ("diag", "cycles")}
+    out["cycles"] = {"choose": info.cycles[0], "query": info.cycles[1],
+                     "update": info.cycles[2], "retire": info.cycles[3]}
+    out["diag"] = {"scans": info.diag[0], "passes": info.diag[1], "segments": info.diag[2],
+                   "edge_rows": info.diag[3]}
+    return out
 
 
 def solve_bestfit_arrays(alloc, free, size, *, device: int = 0, stream: int = 0,

@@ -1,11 +1,10 @@
-// K1/K2 — best-fit skyline planner on sm_100a ("sorted-skyline warp engine").
+// K1/K2 — best-fit skyline planner on sm_100a ("skeleton engine", v6).
 //
 // Replaces solve_bestfit (bestfit.py:276-309) with OffsetLineSet
 // (bestfit.py:61-201) and _RemainingBlocks.take_best (bestfit.py:243-262).
 // Output is bit-identical to the reference: same offset per id, same peak.
 //
-// One warp owns one trace and runs the reference's dependent step loop; all
-// lanes execute every step uniformly (no single-lane pointer chasing):
+// One CTA owns one trace and runs the reference's dependent step loop.
 //
 //  skyline   lines kept as a compact, time-sorted array: line i spans
 //            [LO[i], LO[i+1]) at height H[i]; LOP[i] is the first (alloc,id)
@@ -13,19 +12,29 @@
 //            (t_hi, n).  Heights are in units of the trace's size gcd, so for
 //            all realistic traces they fit 32 bits and (H, LO) packs into one
 //            u64 argmin key.
-//  choose    rule R3 (bestfit.py:115-122): warp argmin of (height, lo) —
-//            per-lane min over strided lines + two redux.sync.min.
+//  choose    rule R3 (bestfit.py:115-122): warp argmin of (height, lo).
+//            Skipped after a placement that leaves a shoulder (the shoulder
+//            is the new lowest-leftmost line).
 //  query     rule R4 (bestfit.py:243-256): the window is positions
-//            [LOP[c], LOP[c+1]); a block fits iff its free rank <= hi.
-//            Entries at positions >= LOP[c+1] can never fit (alloc >= hi), so
-//            only the window's left edge needs a position mask.  Full 32-entry
-//            chunks are answered from a per-chunk summary (min/max free rank
-//            of live entries, best live priority): all-fit -> summary, none
-//            -> skip, straddling -> scanned by the whole warp.  The winner is
-//            the minimum priority rank = max (lifetime, size, -id).
+//            [LOP[c], LOP[c+1]); a block fits iff its free rank <= hi.  Whole
+//            chunks are answered from the shared-memory chunk skeleton
+//            (plan_types.cuh): none fits / the chunk's best entry fits ->
+//            exact answer; otherwise the skeleton names the one 8-slot
+//            segment where the fitting prefix ends, and that segment is
+//            read from the table (two 32-byte sectors) only if its prefix
+//            minimum can still beat the lane's best.  All such segment reads
+//            of a step are issued together (one memory round), overlapped
+//            with the prefetch of the provisional winner's record.  The
+//            partial left chunk is read as one row.  Winner = minimum
+//            priority rank = max (lifetime, size, -id).
 //  update    place (R6, :149-178) and lift_up (R5, :180-201) both replace
 //            the chosen line (and at most one right neighbour) by <= 3 lines;
-//            the tail shifts by d in [-2, 2] with warp-parallel copies.
+//            the tail shifts by d in [-2, 2] with warp-parallel copies.  The
+//            winner's table slot is retired and its chunk skeleton rebuilt
+//            (one row read, overlapped with the skyline update).
+//
+// NW = 1: one warp, no block barriers at all.  NW > 1: warp 0 leads
+// (choose + update), all warps split the window; two barriers per step.
 //
 // The loop bound assert (R8, bestfit.py:297) and IllegalLift (:185-186)
 // are reported through the per-trace status word.
@@ -45,11 +54,22 @@ namespace mp {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr int kPendCap = 256;  // pending segment slots per warp (shared memory)
+
+// Shared-memory tiers for the window structures.
+enum { TIER_GLOBAL = 0, TIER_SKEL = 1, TIER_ALL = 2 };
 
 struct PlanArgs {
     const int64_t *trace_ptr;
-    uint32_t *sf, *sp, *pm;   // chunk-sorted window table (global), 32 per chunk
+    uint32_t *sf, *sp;        // chunk-sorted window table (global), 32 per chunk
+    uint4 *s0, *s1;           // chunk skeleton (global), see plan_types.cuh
+    uint32_t *s2;
+    uint4 *gs;                // group skeleton (global)
+    uint32_t *cnt;            // live entries per chunk (STATS)
     const Rec *rec;           // N
+    const uint2 *raw2;        // N (priority order): raw alloc/free relative to tmin
+    const int64_t *tspan;     // T: raw time span (lifetime pruning when < 2^31)
     const uint32_t *U;        // T
     const int64_t *unit;      // T
     int64_t *offsets;         // N (id order per trace)
@@ -57,10 +77,9 @@ struct PlanArgs {
     int64_t *stats;           // T * ST_N
     const int32_t *tlist;     // optional subset of traces (grid = its length)
     unsigned char *lines_g;   // global line storage when !LINES_SMEM
-    uint4 *summ_g;            // global chunk summaries when !summ_smem
     int lcap;                 // line slots per trace (excluding sentinel)
-    int summ_smem;            // chunk summaries in shared memory
     int rec_smem;             // winner records in shared memory
+    int timing;               // diagnostics: per-phase clock() sums (NW = 1)
 };
 
 __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -103,112 +122,282 @@ template <> struct KeyT<uint64_t> {
     }
 };
 
-// One skyline line: packed (height, lo) key and LOP, 16 B (32 B for wide keys)
+// One skyline line: packed (height, lo) key, LOP and the raw time of lo
+// relative to the trace origin (lifetime pruning); 16 B (32 B for wide keys)
 template <typename K> struct __align__(16) LineRec {
     K key;
     uint32_t lop;
+    uint32_t raw;
 };
 
-// Chunk-sorted window table views (see plan_types.cuh).
-struct Tab {
-    uint32_t *sf, *sp, *pm;
+// Window structures of one trace (pointers already offset to its chunks).
+struct Win {
+    uint4 *s0, *s1;      // chunk skeleton (shared or global)
+    uint32_t *s2;
+    uint4 *gs;           // group skeleton (shared or global)
+    int nch;             // chunks of this trace
+    uint32_t *sf, *sp;   // chunk-sorted table (shared or global)
+    uint32_t *cnt;       // live count per chunk (global, STATS only)
 };
 
-// Mark the winner's slot dead, recompute the chunk's prefix minima and its
-// summary (one warp).  rpos is the winner's (alloc,id) position.
-__device__ __forceinline__ void retire_entry(const Tab &tb, uint4 *summ, uint32_t rpos, int lane) {
-    const int j = (int)(rpos >> 5);
-    const uint32_t key = tb.sf[32 * j + lane];
-    uint32_t pr = tb.sp[32 * j + lane];
-    if ((key & 31u) == (rpos & 31u) && key != 0xFFFFFFFFu) {
-        pr = kDead;
-        tb.sp[32 * j + lane] = kDead;
-    }
-    uint32_t m = pr;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(kFull, m, o);
-        if (lane >= o) m = min(m, v);
-    }
-    tb.pm[32 * j + lane] = m;
-    const unsigned live = __ballot_sync(kFull, pr != kDead);
-    const uint32_t fr = key >> 5;
-    const uint32_t mn = live ? __shfl_sync(kFull, fr, __ffs(live) - 1) : 0xFFFFFFFFu;
-    const uint32_t mx = live ? __shfl_sync(kFull, fr, 31 - __clz(live)) : 0u;
-    const uint32_t bp = __shfl_sync(kFull, m, 31);
-    if (lane == 0) summ[j] = make_uint4(mn, mx, bp, (uint32_t)__popc(live));
+// Issue the row read of the retired entry's chunk (the data is consumed by
+// retire_finish, so the latency overlaps whatever the warp does between).
+struct RetireRow {
+    uint32_t key, pr;
+    int j;
+};
+
+__device__ __forceinline__ RetireRow retire_load(const Win &w, uint32_t pos, int lane) {
+    RetireRow r;
+    r.j = (int)(pos >> 5);
+    r.key = w.sf[32 * r.j + lane];
+    r.pr = w.sp[32 * r.j + lane];
+    return r;
 }
 
-// Step state shared between the leader warp and the query warps.
+// Mark the entry at (alloc,id)-position `pos` dead and rebuild its chunk's
+// skeleton (one warp).
+template <bool STATS>
+__device__ __forceinline__ void retire_finish(const Win &w, RetireRow r, uint32_t pos, int lane) {
+    if ((r.key & 31u) == (pos & 31u) && r.key != kNone) {
+        r.pr = kDead;
+        w.sp[32 * r.j + lane] = kDead;
+    }
+    const uint32_t nlive = skel_store(r.key, r.pr, lane, w.s0, w.s1, w.s2, r.j);
+    if (STATS && lane == 0) w.cnt[r.j] = nlive;
+    __syncwarp();
+    group_store(w.s0, w.nch, w.gs, r.j >> 5, lane);
+}
+
+// Step state shared between the leader warp and the query warps (NW > 1).
 template <typename K> struct StepShared {
-    K ck;                 // chosen line key
-    uint32_t clop, chip;  // chosen line window [clop, chip)
-    uint32_t chi;         // chosen line hi (free-rank threshold)
-    int done;             // loop exit flag (set by the leader)
-    uint32_t wbest[32];   // per-warp best priority rank
-    uint4 wrec[32][2];    // per-warp prefetched winner record
-    unsigned long long wlive[32];
+    uint32_t clop, chip, chi;  // chosen line window [clop, chip), hi
+    uint32_t rawhi;            // raw time of hi (relative)
+    int done;                  // loop exit flag (set by the leader)
+    uint32_t wbest[32];        // per-warp best priority rank
+    uint4 wrec[32][2];         // per-warp prefetched winner record
+    uint2 wraw[32];            // and its raw alloc/free
+    unsigned long long wst[32][5];  // per-warp STATS counters
 };
 
-// Best contained block among the window chunks this warp handles.
-//  - left partial chunk c0 (warp 0, cooperative): slots whose position is
-//    below clop are outside the window;
-//  - every other chunk j in (c0, c1] (one lane each): summary says none /
-//    all fit, or it straddles and a 5-step binary search over the chunk's
-//    sorted free ranks gives the fitting prefix, whose best priority is
-//    PM[count-1].  Positions >= chip can never fit (alloc >= hi), so the
-//    right end needs no mask.
-template <bool STATS, int NW>
-__device__ __forceinline__ uint32_t query_window(const uint4 *summ, const Tab &tb, int c0, int c1,
-                                                 uint32_t chi, uint32_t clop, uint32_t chip,
-                                                 int warp, int lane, unsigned long long &wlive) {
-    uint32_t best = 0xFFFFFFFFu;
-    const uint32_t thr = (chi << 5) | 31u;
-    if (warp == 0) {
-        const uint32_t key = tb.sf[32 * c0 + lane];
-        const uint32_t pr = tb.sp[32 * c0 + lane];
-        const uint32_t slot = key & 31u;
-        if (slot >= (clop & 31u) && key <= thr) best = pr;
-        if (STATS) {
-            const uint32_t pos = 32u * (uint32_t)c0 + slot;
-            wlive += __popc(__ballot_sync(kFull, key != 0xFFFFFFFFu && pr != kDead &&
-                                                     pos >= clop && pos < chip));
-            if (c1 > c0) {
-                const uint32_t k2 = tb.sf[32 * c1 + lane];
-                const uint32_t p2 = tb.sp[32 * c1 + lane];
-                const uint32_t pos2 = 32u * (uint32_t)c1 + (k2 & 31u);
-                wlive += __popc(__ballot_sync(kFull, k2 != 0xFFFFFFFFu && p2 != kDead && pos2 < chip));
+__device__ __forceinline__ uint32_t fit_min4(uint4 k, uint4 v, uint32_t thr, uint32_t best) {
+    best = k.x <= thr ? min(best, v.x) : best;
+    best = k.y <= thr ? min(best, v.y) : best;
+    best = k.z <= thr ? min(best, v.z) : best;
+    best = k.w <= thr ? min(best, v.w) : best;
+    return best;
+}
+
+// Read the pending segments — one per lane, two per lane in flight (64 per
+// wave), each as two 16-byte loads of SF and two of SP — skipping segments
+// whose prefix minimum cannot beat `bound`, which tightens after every wave.
+// Returns this lane's best fitting priority.
+__device__ __forceinline__ uint32_t drain_pending(const Win &w, const uint32_t *pend, int np,
+                                                  uint32_t thr, uint32_t bound, int lane) {
+    __syncwarp();
+    uint32_t best = kNone;
+    for (int e0 = 0; e0 < np; e0 += 64) {
+        uint4 k[2][2], v[2][2];
+        bool act[2];
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const int e = e0 + 32 * u + lane;
+            act[u] = e < np && pend[kPendCap + e] < bound;
+            if (act[u]) {
+                const uint32_t code = pend[e];
+                const int idx = 32 * (int)(code >> 2) + 8 * (int)(code & 3u);
+                const uint4 *kp = reinterpret_cast<const uint4 *>(w.sf + idx);
+                const uint4 *vp = reinterpret_cast<const uint4 *>(w.sp + idx);
+                k[u][0] = kp[0];
+                k[u][1] = kp[1];
+                v[u][0] = vp[0];
+                v[u][1] = vp[1];
             }
         }
-    }
-    for (int jb = c0 + 1 + 32 * warp; jb <= c1; jb += 32 * NW) {
-        const int j = jb + lane;
-        if (STATS) {
-            const uint32_t w = (j < c1) ? summ[j].w : 0u;
-            wlive += __reduce_add_sync(kFull, w);
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            if (act[u]) {
+                best = fit_min4(k[u][0], v[u][0], thr, best);
+                best = fit_min4(k[u][1], v[u][1], thr, best);
+            }
         }
-        if (j <= c1) {
-            const uint4 sm = summ[j];
-            if (sm.x <= chi) {
-                if (sm.y <= chi) {
-                    best = min(best, sm.z);
+        if (e0 + 64 < np) bound = min(bound, __reduce_min_sync(kFull, best));
+    }
+    __syncwarp();
+    return best;
+}
+
+// STATS counters per warp: live window entries, skeleton passes, table
+// segments read, edge rows read.
+struct QStats {
+    unsigned long long wlive = 0, pass = 0, seg = 0, edge = 0;
+};
+
+// Evaluate chunk j against threshold thr from its skeleton: exact answers
+// fold into `best`; a straddling chunk whose boundary segment may still win
+// is appended to the warp's pending list (code = j<<2 | segment, and the
+// segment's prefix minimum as the bound it must beat).
+__device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint32_t thr,
+                                           uint32_t &best, uint32_t *pend, int &np, int lane) {
+    bool need = false;
+    uint32_t code = 0, pe = kNone;
+    if (valid) {
+        const uint4 q = w.s0[j];  // {K0, A, P, K15}
+        if (q.x <= thr) {
+            if (q.y <= thr) {
+                best = min(best, q.z);  // the chunk's best live entry fits
+            } else {
+                // the fitting prefix ends inside segment s; pb / pe = prefix
+                // minima before / through segment s
+                const uint4 r = w.s1[j];  // {K7, K23, P7, P15}
+                uint32_t pb, s;
+                if (q.w <= thr) {
+                    if (r.y <= thr) { s = 3; pb = w.s2[j]; pe = q.z; }
+                    else { s = 2; pb = r.w; pe = w.s2[j]; }
                 } else {
-                    const uint32_t *row = tb.sf + 32 * j;
-                    int cnt = row[15] <= thr ? 16 : 0;
-                    cnt += row[cnt + 7] <= thr ? 8 : 0;
-                    cnt += row[cnt + 3] <= thr ? 4 : 0;
-                    cnt += row[cnt + 1] <= thr ? 2 : 0;
-                    cnt += row[cnt] <= thr ? 1 : 0;
-                    if (cnt > 0) best = min(best, tb.pm[32 * j + cnt - 1]);
+                    if (r.x <= thr) { s = 1; pb = r.z; pe = r.w; }
+                    else { s = 0; pb = kNone; pe = r.z; }
+                }
+                best = min(best, pb);  // slots before segment s all fit
+                if (pe < best) {       // segment s may still hold a better fit
+                    need = true;
+                    code = ((uint32_t)j << 2) | s;
                 }
             }
         }
     }
-    return best;
+    const unsigned m = __ballot_sync(kFull, need);
+    if (m) {
+        if (need) {
+            const int at = np + __popc(m & ((1u << lane) - 1u));
+            pend[at] = code;
+            pend[kPendCap + at] = pe;
+        }
+        np += __popc(m);
+    }
 }
 
-template <typename HT, bool TAB_SMEM, bool LINES_SMEM, bool STATS, int NW>
-__global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
+// Best contained block among the window chunks this warp handles (rule R4).
+// Returns the warp-wide minimum priority; `lbest` is this lane's candidate
+// and the lane holding the warp minimum has prefetched its record into r0/r1.
+template <bool STATS, int NW>
+__device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4, const uint2 *raw2,
+                                                 uint32_t *pend, int c0, int c1, uint32_t chi,
+                                                 uint32_t clop, uint32_t chip, uint32_t rawhi,
+                                                 bool prune, int warp, int lane, uint32_t &lbest,
+                                                 uint4 &r0, uint4 &r1, uint2 &rw, QStats &qs) {
+    const uint32_t thr = (chi << 5) | 31u;
+    uint32_t best = kNone;
+    const bool partial = (clop & 31u) != 0;
+    const int cs = partial ? c0 + 1 : c0;
+    // left edge chunk (warp 0): issue the row read now, consume at the end
+    bool edge = false;
+    uint32_t ek = kNone, ep = kDead;
+    if (warp == 0 && partial && w.s0[c0].x <= thr) {
+        edge = true;
+        ek = w.sf[32 * c0 + lane];
+        ep = w.sp[32 * c0 + lane];
+        if (STATS) qs.edge++;
+    }
+    if (STATS) {
+        // live entries of the reference's window: edge chunk rows (warp 0)
+        // plus the live counts of the chunks strictly inside
+        if (warp == 0) {
+            for (int e = 0; e < (c1 > c0 ? 2 : 1); e++) {
+                const int cc = e ? c1 : c0;
+                const uint32_t kk = w.sf[32 * cc + lane], pp = w.sp[32 * cc + lane];
+                const uint32_t pos = 32u * (uint32_t)cc + (kk & 31u);
+                qs.wlive += __popc(__ballot_sync(kFull, kk != kNone && pp != kDead &&
+                                                            pos >= clop && pos < chip));
+            }
+        }
+        for (int jb = c0 + 1 + 32 * warp; jb < c1; jb += 32 * NW) {
+            const int j = jb + lane;
+            qs.wlive += __reduce_add_sync(kFull, j < c1 ? w.cnt[j] : 0u);
+        }
+    }
+    int np = 0;
+    // chunks of the left partial group (warp 0)
+    const int gcs = cs >> 5;
+    int gf = gcs;
+    if (cs <= c1 && (cs & 31)) {
+        gf = gcs + 1;
+        if (warp == 0) {
+            const int j = cs + lane;
+            if (STATS) qs.pass++;
+            eval_chunk(w, j, j <= c1 && j < 32 * gf, thr, best, pend, np, lane);
+        }
+    }
+    // whole groups [gf, c1 >> 5] (none when the window is the edge chunk alone)
+    const int gl = cs <= c1 ? c1 >> 5 : gf - 1;
+    for (int gb = gf + 32 * warp; gb <= gl; gb += 32 * NW) {
+        const int g = gb + lane;
+        bool scan = false;
+        uint32_t graw = 0;
+        if (STATS) qs.pass++;
+        if (g <= gl) {
+            const uint4 G = w.gs[g];  // {G0, GA, GP, GR}
+            if (G.x <= thr) {
+                if (G.y <= thr) best = min(best, G.z);  // the group's best entry fits
+                else { scan = true; graw = G.w; }
+            }
+        }
+        unsigned m = __ballot_sync(kFull, scan);
+        if (prune && __popc(m) >= 3) {
+            // Lifetime bound: a block of group g that fits [lo, hi) lives at
+            // most rawhi - GR(g).  Priority order is lifetime-major, so a
+            // group whose bound is below the lifetime of the best candidate
+            // so far cannot hold a better one (equal bounds are kept: size
+            // and id break lifetime ties).
+            const uint32_t e = __reduce_min_sync(kFull, best);
+            if (e != kNone) {
+                const uint2 er = raw2[e];
+                const uint32_t lstar = er.y - er.x;
+                m = __ballot_sync(kFull, scan && rawhi - graw >= lstar);
+            }
+        }
+        while (m) {
+            const int g2 = gb + __ffs(m) - 1;
+            m &= m - 1;
+            const int j = 32 * g2 + lane;
+            if (STATS) qs.pass++;
+            eval_chunk(w, j, j <= c1, thr, best, pend, np, lane);
+            if (np > kPendCap - 32) {
+                if (STATS) qs.seg += np;
+                best = min(best, drain_pending(w, pend, np, thr, kNone, lane));
+                np = 0;
+            }
+        }
+    }
+    // provisional warp winner: prefetch its record while the segments load
+    const uint32_t wb1 = __reduce_min_sync(kFull, best);
+    if (best == wb1 && best != kNone) {
+        r0 = rec4[2 * best];
+        r1 = rec4[2 * best + 1];
+        rw = raw2[best];
+    }
+    uint32_t b2 = kNone;
+    if (np) {
+        if (STATS) {
+            for (int e = lane; e < np; e += 32)
+                qs.seg += __popc(__ballot_sync(__activemask(), pend[kPendCap + e] < wb1));
+        }
+        b2 = drain_pending(w, pend, np, thr, wb1, lane);
+    }
+    if (edge && (ek & 31u) >= (clop & 31u) && ek <= thr) b2 = min(b2, ep);
+    if (b2 < best) best = b2;
+    const uint32_t wb = __reduce_min_sync(kFull, best);
+    if (wb != wb1 && best == wb) {  // a segment or the edge chunk improved it
+        r0 = rec4[2 * best];
+        r1 = rec4[2 * best + 1];
+        rw = raw2[best];
+    }
+    lbest = best;
+    return wb;
+}
+
+template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER>
+__global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     using KO = KeyT<HT>;
     using K = typename KO::K;
     using LR = LineRec<K>;
@@ -224,17 +413,19 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
         if (threadIdx.x == 0) {
             a.peaks[t] = 0;
             st[ST_STEPS] = 0; st[ST_LIFTS] = 0; st[ST_MAXLINES] = 0; st[ST_STATUS] = PS_OK;
-            st[ST_WLIVE] = 0;
+            for (int k = ST_WLIVE; k < ST_N; k++) st[k] = 0;
         }
         return;
     }
     const int lcap = a.lcap;
+    const bool prune = a.tspan[t] < (int64_t(1) << 31);
     const int nch = (n + 31) >> 5;
     const int64_t unit = a.unit[t];
     const int64_t cb = chunk_base(base, t);
-    unsigned long long wlive = 0;  // STATS: live entries in the reference's windows
+    QStats qs;                     // STATS counters (this warp)
+    unsigned long long nscan = 0;  // STATS: choose scans (leader)
 
-    // ---- carve shared memory: lines | summaries | table | records ----
+    // ---- carve shared memory: lines | pending | skeleton | table | records ----
     size_t off = 0;
     LR *L;
     {
@@ -242,34 +433,51 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
         L = reinterpret_cast<LR *>(LINES_SMEM ? smem : a.lines_g + (size_t)blockIdx.x * stride);
         if (LINES_SMEM) off = stride;
     }
-    uint4 *summ;
-    if (a.summ_smem) {
-        summ = reinterpret_cast<uint4 *>(smem + off);
-        off += (size_t)nch * sizeof(uint4);
-        const uint4 *src = a.summ_g + cb;
-        for (int i = threadIdx.x; i < nch; i += 32 * NW) summ[i] = src[i];
+    uint32_t *pend = reinterpret_cast<uint32_t *>(smem + off) + warp * 2 * kPendCap;
+    off += (size_t)NW * 2 * kPendCap * sizeof(uint32_t);
+    Win win;
+    win.cnt = a.cnt + cb;
+    win.nch = nch;
+    const int ngr = (nch + 31) >> 5;
+    const int64_t gbase = group_base(base, t);
+    if (TIER >= TIER_SKEL) {
+        uint4 *g = reinterpret_cast<uint4 *>(smem + off);
+        off += (size_t)ngr * 16;
+        for (int i = threadIdx.x; i < ngr; i += 32 * NW) g[i] = a.gs[gbase + i];
+        win.gs = g;
     } else {
-        summ = a.summ_g + cb;
+        win.gs = a.gs + gbase;
     }
-    Tab tb;
-    if (TAB_SMEM) {
+    if (TIER >= TIER_SKEL) {
+        uint4 *d = reinterpret_cast<uint4 *>(smem + off);
+        off += (size_t)nch * 32 + align16((size_t)nch * 4);
+        for (int i = threadIdx.x; i < nch; i += 32 * NW) {
+            d[i] = a.s0[cb + i];
+            d[nch + i] = a.s1[cb + i];
+            reinterpret_cast<uint32_t *>(d + 2 * nch)[i] = a.s2[cb + i];
+        }
+        win.s0 = d;
+        win.s1 = d + nch;
+        win.s2 = reinterpret_cast<uint32_t *>(d + 2 * nch);
+    } else {
+        win.s0 = a.s0 + cb;
+        win.s1 = a.s1 + cb;
+        win.s2 = a.s2 + cb;
+    }
+    if (TIER == TIER_ALL) {
         uint32_t *d = reinterpret_cast<uint32_t *>(smem + off);
-        tb.sf = d;
-        tb.sp = d + 32 * nch;
-        tb.pm = d + 64 * nch;
-        off += (size_t)nch * 32 * 12;
+        off += (size_t)nch * 32 * 8;
         const uint4 *s0 = reinterpret_cast<const uint4 *>(a.sf + 32 * cb);
         const uint4 *s1 = reinterpret_cast<const uint4 *>(a.sp + 32 * cb);
-        const uint4 *s2 = reinterpret_cast<const uint4 *>(a.pm + 32 * cb);
         for (int i = threadIdx.x; i < nch * 8; i += 32 * NW) {
-            reinterpret_cast<uint4 *>(tb.sf)[i] = s0[i];
-            reinterpret_cast<uint4 *>(tb.sp)[i] = s1[i];
-            reinterpret_cast<uint4 *>(tb.pm)[i] = s2[i];
+            reinterpret_cast<uint4 *>(d)[i] = s0[i];
+            reinterpret_cast<uint4 *>(d + 32 * nch)[i] = s1[i];
         }
+        win.sf = d;
+        win.sp = d + 32 * nch;
     } else {
-        tb.sf = a.sf + 32 * cb;
-        tb.sp = a.sp + 32 * cb;
-        tb.pm = a.pm + 32 * cb;
+        win.sf = a.sf + 32 * cb;
+        win.sp = a.sp + 32 * cb;
     }
     const uint4 *rec4;
     if (a.rec_smem) {
@@ -282,8 +490,9 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
     }
     // R2: one line over the whole span at height 0 (bestfit.py:287-289)
     if (threadIdx.x == 0) {
-        L[0].key = KO::make(0, 0); L[0].lop = 0;
+        L[0].key = KO::make(0, 0); L[0].lop = 0; L[0].raw = 0;
         L[1].key = KO::make(0, a.U[t] - 1); L[1].lop = (uint32_t)n;  // sentinel
+        L[1].raw = prune ? (uint32_t)a.tspan[t] : 0u;
         ss.done = 0;
     }
     __syncthreads();
@@ -302,8 +511,10 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
     K ck = KO::make(0, 0);
     HT hP = 0, hN = 0;
     bool hasP = false, hasN = false;
-    uint32_t clop = 0, chip = 0, chi = 0;
+    uint32_t clop = 0, chip = 0, chi = 0, craw = 0, rawhi = 0;
 
+    long long tph[4] = {0, 0, 0, 0};  // timing: choose, query, update, retire
+    long long tc = a.timing ? clock64() : 0;
     for (;;) {
         // ======== leader: choose (R3) ========
         if (warp == 0) {
@@ -312,79 +523,87 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
                 if (lane == 0) ss.done = 1;
             } else {
                 if (!known) {
-                    K bk = KO::none();
-                    int bi = 0;
-                    for (int i0 = lane; i0 < nl; i0 += 128) {
+                    if (STATS) nscan++;
+                    if (nl <= 32) {
+                        const K k = lane < nl ? L[lane].key : KO::none();
+                        ck = KO::warp_min(k);
+                        c = __ffs(__ballot_sync(kFull, k == ck)) - 1;
+                    } else {
+                        K bk = KO::none();
+                        int bi = 0;
+                        for (int i0 = lane; i0 < nl; i0 += 128) {
 #pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const int i = i0 + 32 * u;
-                            const K k = i < nl ? L[i].key : KO::none();
-                            if (k < bk) { bk = k; bi = i; }
+                            for (int u = 0; u < 4; u++) {
+                                const int i = i0 + 32 * u;
+                                const K k = i < nl ? L[i].key : KO::none();
+                                if (k < bk) { bk = k; bi = i; }
+                            }
                         }
+                        ck = KO::warp_min(bk);
+                        c = __shfl_sync(kFull, bi, __ffs(__ballot_sync(kFull, bk == ck)) - 1);
                     }
-                    ck = KO::warp_min(bk);
-                    c = __shfl_sync(kFull, bi, __ffs(__ballot_sync(kFull, bk == ck)) - 1);
                 }
                 hasP = c > 0;
                 hasN = c + 1 < nl;
                 const LR ln = L[c + 1];
                 const K kp = hasP ? L[c - 1].key : KO::none();
                 clop = L[c].lop;
+                craw = L[c].raw;
+                rawhi = ln.raw;
                 chip = ln.lop;
                 chi = KO::lo(ln.key);
                 hN = KO::h(ln.key);
                 hP = KO::h(kp);
                 if (NW > 1 && lane == 0) {
-                    ss.clop = clop; ss.chip = chip; ss.chi = chi;
+                    ss.clop = clop; ss.chip = chip; ss.chi = chi; ss.rawhi = rawhi;
                 }
             }
         }
         if (NW > 1) __syncthreads();  // [A] choice published
         if (NW > 1 ? ss.done : (placed >= n || status != PS_OK)) break;
 
+        if (a.timing) { const long long t2 = clock64(); tph[0] += t2 - tc; tc = t2; }
         // ======== all warps: query (R4) ========
-        uint32_t qlop, qhip, qchi;
-        if (NW > 1) { qlop = ss.clop; qhip = ss.chip; qchi = ss.chi; }
-        else { qlop = clop; qhip = chip; qchi = chi; }
-        uint32_t best = 0xFFFFFFFFu;
+        uint32_t qlop, qhip, qchi, qraw;
+        if (NW > 1) { qlop = ss.clop; qhip = ss.chip; qchi = ss.chi; qraw = ss.rawhi; }
+        else { qlop = clop; qhip = chip; qchi = chi; qraw = rawhi; }
+        uint32_t lbest = kNone, wb = kNone;
+        uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
+        uint2 rw = make_uint2(0, 0);
         if (qlop < qhip) {
             const int c0 = (int)(qlop >> 5), c1 = (int)((qhip - 1) >> 5);
-            best = query_window<STATS, NW>(summ, tb, c0, c1, qchi, qlop, qhip, warp, lane, wlive);
+            wb = query_window<STATS, NW>(win, rec4, a.raw2 + base, pend, c0, c1, qchi, qlop, qhip,
+                                         qraw, prune, warp, lane, lbest, r0, r1, rw, qs);
         }
-        // every lane prefetches its own candidate's record before the
-        // reductions, so the L2 latency overlaps them and barrier [B]
-        uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
-        if (best != 0xFFFFFFFFu) {
-            r0 = rec4[2 * best];
-            r1 = rec4[2 * best + 1];
-        }
-        const uint32_t wb = __reduce_min_sync(kFull, best);
         uint32_t gbest;
         if (NW > 1) {
-            if (best == wb && best != 0xFFFFFFFFu) {
+            if (lbest == wb && wb != kNone) {
                 ss.wrec[warp][0] = r0;
                 ss.wrec[warp][1] = r1;
+                ss.wraw[warp] = rw;
             }
             if (lane == 0) ss.wbest[warp] = wb;
             __syncthreads();  // [B] per-warp winners published
-            const uint32_t mine = lane < NW ? ss.wbest[lane] : 0xFFFFFFFFu;
+            const uint32_t mine = lane < NW ? ss.wbest[lane] : kNone;
             gbest = __reduce_min_sync(kFull, mine);
             int ww = -1;
-            if (gbest != 0xFFFFFFFFu) ww = __ffs(__ballot_sync(kFull, mine == gbest)) - 1;
+            if (gbest != kNone) ww = __ffs(__ballot_sync(kFull, mine == gbest)) - 1;
             if (ww == warp) {
                 // the winning warp retires the entry while the leader
-                // rewrites the skyline
-                retire_entry(tb, summ, ss.wrec[warp][0].x, lane);
+                // rewrites the skyline (both finish before barrier [A])
+                const uint32_t pos = ss.wrec[warp][0].x;
+                retire_finish<STATS>(win, retire_load(win, pos, lane), pos, lane);
             }
             if (warp != 0) continue;
-            if (gbest != 0xFFFFFFFFu) {
+            if (gbest != kNone) {
                 r0 = ss.wrec[ww][0];
                 r1 = ss.wrec[ww][1];
+                rw = ss.wraw[ww];
             }
         } else {
             gbest = wb;
-            if (gbest != 0xFFFFFFFFu) {
-                const int src = __ffs(__ballot_sync(kFull, best == gbest)) - 1;
+            if (gbest != kNone) {
+                const int src = __ffs(__ballot_sync(kFull, lbest == gbest)) - 1;
                 r0.x = __shfl_sync(kFull, r0.x, src);
                 r0.y = __shfl_sync(kFull, r0.y, src);
                 r0.z = __shfl_sync(kFull, r0.z, src);
@@ -393,14 +612,18 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
                 r1.y = __shfl_sync(kFull, r1.y, src);
                 r1.z = __shfl_sync(kFull, r1.z, src);
                 if (sizeof(HT) == 8) r1.w = __shfl_sync(kFull, r1.w, src);
+                rw.x = __shfl_sync(kFull, rw.x, src);
+                rw.y = __shfl_sync(kFull, rw.y, src);
             }
         }
 
+        if (a.timing) { const long long t2 = clock64(); tph[1] += t2 - tc; tc = t2; }
         // ======== leader: replacement of lines [c, c+e] by m new lines ========
         K nk0 = 0, nk1 = 0, nk2 = 0;
-        uint32_t np0 = 0, np1 = 0, np2 = 0;
+        uint32_t np0 = 0, np1 = 0, np2 = 0, nr0 = 0, nr1 = 0, nr2 = 0;
         int m = 0, e = 0, cnext = c;
-        if (gbest == 0xFFFFFFFFu) {
+        RetireRow rr{};
+        if (gbest == kNone) {
             // lift_up (R5)
             ++lifts;
             if (!hasP && !hasN) {
@@ -414,11 +637,13 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
             m = intoN ? 1 : 0;
             nk0 = KO::make(hN, KO::lo(ck));
             np0 = clop;
+            nr0 = craw;
             known = false;
         } else {
             // place (R6)
             const uint32_t rpos = r0.x, rar = r0.y, rfr = r0.z, rap = r0.w, rfp = r1.x,
                            rk = r1.y;
+            if (NW == 1) rr = retire_load(win, rpos, lane);  // overlaps the update
             HT rsz = (HT)r1.z;
             if (sizeof(HT) == 8) rsz |= (HT)((uint64_t)r1.w << 32);
             const HT ch = KO::h(ck);
@@ -427,7 +652,6 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
             if (lane == 0) a.offsets[base + rk] = (int64_t)ch * unit;
             peak = max(peak, newh);
             ++placed;
-            if (NW == 1) retire_entry(tb, summ, rpos, lane);
             const bool hasL = clo < rar, hasR = rfr < chi;
             const bool mP = !hasL && hasP && hP == newh;  // flush re-merge (:171-174)
             const bool mN = !hasR && hasN && hN == newh;  // (:175-177)
@@ -436,10 +660,13 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
             // sequence: [L?] [raised unless merged into P] [R?]
             nk0 = hasL ? kL : (!mP ? kRa : kR);
             np0 = hasL ? clop : (!mP ? rap : rfp);
+            nr0 = hasL ? craw : (!mP ? rw.x : rw.y);
             nk1 = hasL ? (!mP ? kRa : kR) : kR;
             np1 = hasL ? (!mP ? rap : rfp) : rfp;
+            nr1 = hasL ? (!mP ? rw.x : rw.y) : rw.y;
             nk2 = kR;
             np2 = rfp;
+            nr2 = rw.y;
             m = (hasL ? 1 : 0) + (mP ? 0 : 1) + (hasR ? 1 : 0);
             known = hasL || hasR;
             ck = hasL ? kL : kR;
@@ -454,7 +681,15 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
             placed = n;
             continue;
         }
-        if (d != 0) {
+        if (d != 0 && nl < 32) {
+            const int from = c + 1 + e;  // lines [from, nl] (incl. sentinel) move by d
+            const bool mv = lane >= from && lane <= nl;
+            LR v;
+            if (mv) v = L[lane];
+            __syncwarp();
+            if (mv) L[lane + d] = v;
+            __syncwarp();
+        } else if (d != 0) {
             const int from = c + 1 + e, to = nl;  // inclusive
             const int nblk = (to - from) >> 7;
             for (int q = 0; q <= nblk; q++) {
@@ -479,18 +714,28 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
             LR v;
             v.key = lane == 0 ? nk0 : (lane == 1 ? nk1 : nk2);
             v.lop = lane == 0 ? np0 : (lane == 1 ? np1 : np2);
+            v.raw = lane == 0 ? nr0 : (lane == 1 ? nr1 : nr2);
             L[c + lane] = v;
         }
         nl += d;
         maxl = max(maxl, nl);
         c = cnext;
+        if (a.timing) { const long long t2 = clock64(); tph[2] += t2 - tc; tc = t2; }
+        if (NW == 1 && gbest != kNone) retire_finish<STATS>(win, rr, r0.x, lane);
         __syncwarp();
+        if (a.timing) { const long long t2 = clock64(); tph[3] += t2 - tc; tc = t2; }
     }
     if (STATS && NW > 1) {
-        if (lane == 0) ss.wlive[warp] = wlive;
+        if (lane == 0) {
+            ss.wst[warp][0] = qs.wlive; ss.wst[warp][1] = qs.pass;
+            ss.wst[warp][2] = qs.seg; ss.wst[warp][3] = qs.edge;
+        }
         __syncthreads();
         if (threadIdx.x == 0)
-            for (int w = 1; w < NW; w++) wlive += ss.wlive[w];
+            for (int w = 1; w < NW; w++) {
+                qs.wlive += ss.wst[w][0]; qs.pass += ss.wst[w][1];
+                qs.seg += ss.wst[w][2]; qs.edge += ss.wst[w][3];
+            }
     }
     if (threadIdx.x == 0) {
         a.peaks[t] = (int64_t)peak * unit;  // R7: max(offset + size)
@@ -498,7 +743,12 @@ __global__ void __launch_bounds__(32 * NW) k_plan_sorted(PlanArgs a) {
         st[ST_LIFTS] = lifts;
         st[ST_MAXLINES] = maxl;
         st[ST_STATUS] = status;
-        st[ST_WLIVE] = (int64_t)wlive;
+        st[ST_WLIVE] = (int64_t)qs.wlive;
+        st[ST_SCAN] = (int64_t)nscan;
+        st[ST_PASS] = (int64_t)qs.pass;
+        st[ST_SEG] = (int64_t)qs.seg;
+        st[ST_EDGE] = (int64_t)qs.edge;
+        for (int k = 0; k < 4; k++) st[ST_T0 + k] = tph[k];
     }
 }
 
@@ -506,9 +756,9 @@ thread_local int64_t g_launches = 0;
 thread_local int g_nwarps = 1;  // warps per trace chosen by plan_device
 thread_local int g_carveout = -1;  // shared-memory carveout percent (-1: driver default)
 
-template <typename HT, bool E, bool Ls, bool ST, int NW>
-int launch_nw(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
-    auto fn = k_plan_sorted<HT, E, Ls, ST, NW>;
+template <typename HT, bool Ls, bool ST, int NW, int TIER>
+int launch_k(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
+    auto fn = k_plan<HT, Ls, ST, NW, TIER>;
     if (smem > 48 * 1024)
         MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // keep only the shared memory the resident CTAs need: the rest is L1,
@@ -520,33 +770,35 @@ int launch_nw(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
     return MP_OK;
 }
 
+template <typename HT, bool Ls, bool ST, int TIER>
+int launch_nw(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
+    if (g_nwarps == 1) return launch_k<HT, Ls, ST, 1, TIER>(a, grid, smem, s);
+    return launch_k<HT, Ls, ST, 8, TIER>(a, grid, smem, s);
+}
 
-template <typename HT, bool E, bool Ls, bool ST>
-int launch_one(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
-    switch (g_nwarps) {
-        case 1: return launch_nw<HT, E, Ls, ST, 1>(a, grid, smem, s);
-        case 4: return launch_nw<HT, E, Ls, ST, 4>(a, grid, smem, s);
-        case 8: return launch_nw<HT, E, Ls, ST, 8>(a, grid, smem, s);
-        default: return launch_nw<HT, E, Ls, ST, 16>(a, grid, smem, s);
+template <typename HT, bool Ls, bool ST>
+int launch_tier(const PlanArgs &a, int grid, int tier, size_t smem, cudaStream_t s) {
+    switch (tier) {
+        case TIER_ALL: return launch_nw<HT, Ls, ST, TIER_ALL>(a, grid, smem, s);
+        case TIER_SKEL: return launch_nw<HT, Ls, ST, TIER_SKEL>(a, grid, smem, s);
+        default: return launch_nw<HT, Ls, ST, TIER_GLOBAL>(a, grid, smem, s);
     }
 }
 
 template <typename HT, bool ST>
-int launch_ht(const PlanArgs &a, int grid, bool ent_smem, bool lines_smem, size_t smem,
+int launch_ht(const PlanArgs &a, int grid, int tier, bool lines_smem, size_t smem,
               cudaStream_t s) {
-    if (ent_smem && lines_smem) return launch_one<HT, true, true, ST>(a, grid, smem, s);
-    if (ent_smem) return launch_one<HT, true, false, ST>(a, grid, smem, s);
-    if (lines_smem) return launch_one<HT, false, true, ST>(a, grid, smem, s);
-    return launch_one<HT, false, false, ST>(a, grid, smem, s);
+    if (lines_smem) return launch_tier<HT, true, ST>(a, grid, tier, smem, s);
+    return launch_tier<HT, false, ST>(a, grid, tier, smem, s);
 }
 
-int launch_plan(const PlanArgs &a, int grid, bool h32, bool ent_smem, bool lines_smem,
-                size_t smem, cudaStream_t s, bool stats) {
+int launch_plan(const PlanArgs &a, int grid, bool h32, int tier, bool lines_smem, size_t smem,
+                cudaStream_t s, bool stats) {
     if (stats)
-        return h32 ? launch_ht<uint32_t, true>(a, grid, ent_smem, lines_smem, smem, s)
-                   : launch_ht<uint64_t, true>(a, grid, ent_smem, lines_smem, smem, s);
-    return h32 ? launch_ht<uint32_t, false>(a, grid, ent_smem, lines_smem, smem, s)
-               : launch_ht<uint64_t, false>(a, grid, ent_smem, lines_smem, smem, s);
+        return h32 ? launch_ht<uint32_t, true>(a, grid, tier, lines_smem, smem, s)
+                   : launch_ht<uint64_t, true>(a, grid, tier, lines_smem, smem, s);
+    return h32 ? launch_ht<uint32_t, false>(a, grid, tier, lines_smem, smem, s)
+               : launch_ht<uint64_t, false>(a, grid, tier, lines_smem, smem, s);
 }
 
 thread_local mp_plan_info g_info;
@@ -560,32 +812,42 @@ size_t smem_limit(int device) {
 inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct Layout {
-    bool lines_smem, summ_smem, tab_smem, rec_smem;
+    bool lines_smem, rec_smem;
+    int tier;  // TIER_GLOBAL / TIER_SKEL / TIER_ALL
     size_t smem;
 };
 
-// Shared memory priority: skyline lines > chunk summaries > chunk-sorted
-// window table > winner records.
+// Shared memory priority: skyline lines > pending list > chunk skeleton >
+// chunk-sorted window table > winner records.
 // per line: LineRec = packed key + LOP, 16 B (32 B for 64-bit heights)
 size_t lines_bytes(int lcap, size_t hbytes) {
     const size_t lr = hbytes == 4 ? 16 : 32;
     return a16((size_t)(lcap + 1) * lr);
 }
 
-Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, bool force_global,
-                     bool lines_global = false) {
+Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwarps,
+                     bool force_global, bool lines_global = false) {
     Layout l{};
+    l.tier = TIER_GLOBAL;
     const size_t lines_b = lines_bytes(lcap, hbytes);
+    const size_t pend_b = (size_t)nwarps * 2 * kPendCap * sizeof(uint32_t);
     const int64_t nch = (nmax + 31) / 32;
-    const size_t summ_b = (size_t)nch * 16;
-    const size_t tab_b = (size_t)nch * 32 * 12;
+    const size_t skel_b = (size_t)nch * 32 + a16((size_t)nch * 4) + (size_t)((nch + 31) / 32) * 16;
+    const size_t tab_b = (size_t)nch * 32 * 8;
     const size_t rec_b = (size_t)nmax * 32;
-    if (force_global) return l;
-    size_t used = 0;
-    if (!lines_global && lines_b <= lim) { l.lines_smem = true; used += lines_b; }
-    if (used + summ_b <= lim) { l.summ_smem = true; used += summ_b; }
-    if (used + tab_b <= lim) { l.tab_smem = true; used += tab_b; }
-    if (used + rec_b <= lim) { l.rec_smem = true; used += rec_b; }
+    size_t used = pend_b;
+    if (!force_global) {
+        if (!lines_global && used + lines_b <= lim) { l.lines_smem = true; used += lines_b; }
+        if (used + skel_b <= lim) {
+            l.tier = TIER_SKEL;
+            used += skel_b;
+            if (used + tab_b <= lim) {
+                l.tier = TIER_ALL;
+                used += tab_b;
+                if (used + rec_b <= lim) { l.rec_smem = true; used += rec_b; }
+            }
+        }
+    }
     l.smem = used;
     return l;
 }
@@ -611,11 +873,15 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
         return MP_ERR_INVALID;
     }
     const int64_t nchunks = N / 32 + T + 1;
+    const int64_t ngroups = nchunks / 32 + T + 1;
     const size_t prep_b = prep_scratch_bytes(N, T);
     const size_t tab_b = Carver::need<uint2>(N) + Carver::need<Rec>(N) +
                          Carver::need<uint32_t>(T) + Carver::need<int64_t>(T) +
                          Carver::need<uint64_t>(T) + Carver::need<int64_t>(T * ST_N) +
-                         Carver::need<uint4>(nchunks) + 3 * Carver::need<uint32_t>(32 * nchunks);
+                         2 * Carver::need<uint4>(nchunks) + 2 * Carver::need<uint32_t>(nchunks) +
+                         Carver::need<uint4>(ngroups) + Carver::need<uint2>(N) +
+                         Carver::need<uint32_t>(N) + 2 * Carver::need<int64_t>(T) +
+                         2 * Carver::need<uint32_t>(32 * nchunks);
     Scratch sc;
     MP_TRY(sc.alloc(prep_b + tab_b, s));
     Carver cv(sc.ptr, prep_b + tab_b);
@@ -623,14 +889,22 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     po.ent = cv.take<uint2>(N);
     po.sf = cv.take<uint32_t>(32 * nchunks);
     po.sp = cv.take<uint32_t>(32 * nchunks);
-    po.pm = cv.take<uint32_t>(32 * nchunks);
+    po.s0 = cv.take<uint4>(nchunks);
+    po.s1 = cv.take<uint4>(nchunks);
+    po.s2 = cv.take<uint32_t>(nchunks);
+    po.nchunks = nchunks;
+    po.gs = cv.take<uint4>(ngroups);
+    po.ngroups = ngroups;
+    po.cnt = cv.take<uint32_t>(nchunks);
     po.rec = cv.take<Rec>(N);
+    po.raw2 = cv.take<uint2>(N);
+    po.rawpos = cv.take<uint32_t>(N);
+    po.tmin = cv.take<int64_t>(T);
+    po.tspan = cv.take<int64_t>(T);
     po.U = cv.take<uint32_t>(T);
     po.unit = cv.take<int64_t>(T);
     po.total_units = cv.take<uint64_t>(T);
     int64_t *stats = cv.take<int64_t>(T * ST_N);
-    uint4 *summ_g = cv.take<uint4>(nchunks);
-    po.summ = summ_g;
     void *prep_ws = cv.base + cv.off;
     size_t prep_ws_b = cv.cap - cv.off;
 
@@ -651,43 +925,71 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     for (int64_t t = 0; t < T; t++) h32 = h32 && tot[t] < (uint64_t(1) << 32);
     const size_t hb = h32 ? 4 : 8;
 
-    const size_t lim = smem_limit(device);
+    // dynamic shared memory limit (the static StepShared block takes ~1.5 KB)
+    const size_t lim = smem_limit(device) - 2048;
     const bool force_global = (flags & MP_FORCE_GLOBAL) != 0;
     const int64_t lneed = 2 * nmax + 2;  // worst case 2n+1 lines
-    const int lcap_s = (int)std::min<int64_t>(lneed, 2048);
-    Layout lay = choose_layout(nmax, lcap_s, hb, lim, force_global);
-    // warps per trace: one leader warp always; helper warps split the window
-    // query when the entry table lives in L2 (long dependent load chains)
-    g_nwarps = lay.tab_smem ? 1 : 8;
+    // Layout policy.  A single trace (or fewer traces than SMs) gets the
+    // whole shared memory of its SM: latency is what matters.  A large batch
+    // wants several traces resident per SM to hide the step chain's memory
+    // latency, so each CTA is budgeted 1/conc of the SM's shared memory
+    // (conc = traces per SM, capped) and the window structures take the
+    // highest tier that fits that budget.
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int conc = (int)std::min<int64_t>((T + sms - 1) / sms, 8);
+    if (const char *env = getenv("MEMPLAN_CONC")) conc = std::max(1, std::min(32, atoi(env)));
+    const int lcap_s = (int)std::min<int64_t>(lneed, conc > 1 ? 256 : 1024);
+    const size_t budget =
+        conc > 1 ? std::min(lim, (size_t)(228 * 1024) / conc - 1024 - 2048) : lim;
+    g_nwarps = 1;
+    Layout lay = choose_layout(nmax, lcap_s, hb, budget, 1, force_global);
+    if (const char *env = getenv("MEMPLAN_NWARPS")) {
+        const int v = atoi(env);
+        if (v == 1 || v == 8) {
+            g_nwarps = v;
+            lay = choose_layout(nmax, lcap_s, hb, budget, v, force_global);
+        }
+    }
+    if (const char *env = getenv("MEMPLAN_TIER")) {  // tuning: cap the shared-memory tier
+        const int v = atoi(env);
+        if (v >= TIER_GLOBAL && v < lay.tier) {
+            lay = choose_layout(nmax, lcap_s, hb, budget, g_nwarps, force_global);
+            if (v == TIER_GLOBAL) {
+                lay.tier = TIER_GLOBAL;
+                lay.rec_smem = false;
+                lay.smem = lines_bytes(lcap_s, hb) + (size_t)g_nwarps * 2 * kPendCap * 4;
+            }
+        }
+    }
     {
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int64_t per_sm = std::max<int64_t>(1, (T + sms - 1) / sms);
         const double need = (double)per_sm * (double)(lay.smem + 1024 + sizeof(void *) * 256);
         int pct = (int)std::ceil(100.0 * need / (228.0 * 1024.0));
         g_carveout = std::min(100, std::max(0, pct));
-    }
-    if (const char *env = getenv("MEMPLAN_NWARPS")) {
-        const int v = atoi(env);
-        if (v == 1 || v == 4 || v == 8 || v == 16) g_nwarps = v;
     }
 
     PlanArgs a{};
     a.trace_ptr = trace_ptr_d;
     a.sf = po.sf;
     a.sp = po.sp;
-    a.pm = po.pm;
+    a.s0 = po.s0;
+    a.s1 = po.s1;
+    a.s2 = po.s2;
+    a.gs = po.gs;
+    a.cnt = po.cnt;
     a.rec = po.rec;
+    a.raw2 = po.raw2;
+    a.tspan = po.tspan;
     a.U = po.U;
     a.unit = po.unit;
     a.offsets = offsets_d;
     a.peaks = peaks_d;
     a.stats = stats;
     a.tlist = nullptr;
-    a.summ_g = summ_g;
     a.lcap = lay.lines_smem ? lcap_s : (int)lneed;
-    a.summ_smem = lay.summ_smem;
     a.rec_smem = lay.rec_smem;
+    a.timing = getenv("MEMPLAN_TIMING") != nullptr;
     const size_t line_bytes_g = lines_bytes(a.lcap, hb);
     Scratch lines_sc;
     if (!lay.lines_smem) {
@@ -699,7 +1001,7 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     cudaEvent_t k0, k1;
     cudaEventCreate(&k0); cudaEventCreate(&k1);
     cudaEventRecord(k0, s);
-    MP_TRY(launch_plan(a, (int)T, h32, lay.tab_smem, lay.lines_smem, lay.smem, s, stats_on));
+    MP_TRY(launch_plan(a, (int)T, h32, lay.tier, lay.lines_smem, lay.smem, s, stats_on));
     cudaEventRecord(k1, s);
 
     // ---- collect status; re-run overflowed traces with global lines ----
@@ -722,14 +1024,12 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
         PlanArgs b = a;
         b.tlist = tl.as<int32_t>();
         b.lcap = (int)lneed;
-        lay2 = choose_layout(nmax, b.lcap, hb, lim, force_global, /*lines_global=*/true);
-        b.summ_smem = lay2.summ_smem;
+        lay2 = choose_layout(nmax, b.lcap, hb, lim, g_nwarps, force_global, /*lines_global=*/true);
         b.rec_smem = lay2.rec_smem;
         Scratch lg;
         MP_TRY(lg.alloc(redo.size() * lines_bytes(b.lcap, hb), s));
         b.lines_g = lg.as<unsigned char>();
-        MP_TRY(launch_plan(b, (int)redo.size(), h32, lay2.tab_smem, false, lay2.smem, s,
-                           stats_on));
+        MP_TRY(launch_plan(b, (int)redo.size(), h32, lay2.tier, false, lay2.smem, s, stats_on));
         MP_CUDA(cudaMemcpyAsync(hst.data(), stats, sizeof(int64_t) * T * ST_N,
                                 cudaMemcpyDeviceToHost, s));
         MP_CUDA(cudaStreamSynchronize(s));
@@ -747,13 +1047,16 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     g_info.plan_ms = ms_plan;
     g_info.kernel_ms = ms_kernel;
     g_info.launches = prep_launches() + (g_launches - launches0);
-    g_info.engine = (h32 ? 16 : 0) | (lay.lines_smem ? 8 : 0) | (lay.summ_smem ? 4 : 0) |
-                    (lay.tab_smem ? 2 : 0) | (lay.rec_smem ? 1 : 0) | (redo.empty() ? 0 : 32);
+    g_info.engine = (h32 ? 16 : 0) | (lay.lines_smem ? 8 : 0) | (lay.tier >= TIER_SKEL ? 4 : 0) |
+                    (lay.tier == TIER_ALL ? 2 : 0) | (lay.rec_smem ? 1 : 0) |
+                    (redo.empty() ? 0 : 32);
     g_info.cluster = g_nwarps;  // warps per trace (single-CTA engine)
     for (int64_t t = 0; t < T; t++) {
         g_info.steps += hst[t * ST_N + ST_STEPS];
         g_info.lifts += hst[t * ST_N + ST_LIFTS];
         g_info.sum_wlive += hst[t * ST_N + ST_WLIVE];
+        for (int k = 0; k < 4; k++) g_info.diag[k] += hst[t * ST_N + ST_SCAN + k];
+        for (int k = 0; k < 4; k++) g_info.cycles[k] += hst[t * ST_N + ST_T0 + k];
         g_info.max_lines = std::max(g_info.max_lines, hst[t * ST_N + ST_MAXLINES]);
         int64_t stv = hst[t * ST_N + ST_STATUS];
         if (stv == PS_LOOP_BOUND) {

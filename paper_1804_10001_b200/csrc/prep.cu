@@ -180,13 +180,43 @@ __device__ __forceinline__ int64_t gcd64(int64_t a, int64_t b) {
 // Every skyline height is a sum of sizes, hence a multiple of g; when the
 // total is below 2^32 units the planner runs on 32-bit heights and packs
 // (height, lo) into one 64-bit argmin key.
+//
+// Also the trace's time origin tmin = min alloc and span = max free - tmin:
+// raw times relative to tmin feed the planner's lifetime-bound pruning,
+// which is enabled when the span fits 31 bits.
 __global__ void k_trace_scale(const int64_t *__restrict__ trace_ptr,
-                              const int64_t *__restrict__ size, int64_t *__restrict__ unit,
-                              uint64_t *__restrict__ total_units) {
+                              const int64_t *__restrict__ size, const int64_t *__restrict__ alloc,
+                              const int64_t *__restrict__ free_, int64_t *__restrict__ unit,
+                              uint64_t *__restrict__ total_units, int64_t *__restrict__ tmin,
+                              int64_t *__restrict__ tspan) {
     __shared__ int64_t sg[32];
     __shared__ uint64_t ss[32];
+    __shared__ int64_t smn[32], smx[32];
     const int64_t t = blockIdx.x;
     const int64_t b = trace_ptr[t], e = trace_ptr[t + 1];
+    {
+        int64_t mn = INT64_MAX, mx = INT64_MIN;
+        for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+            mn = min(mn, alloc[i]);
+            mx = max(mx, free_[i]);
+        }
+        for (int o = 16; o; o >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+        }
+        if ((threadIdx.x & 31) == 0) { smn[threadIdx.x >> 5] = mn; smx[threadIdx.x >> 5] = mx; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < (int)(blockDim.x >> 5); w++) {
+                mn = min(mn, smn[w]);
+                mx = max(mx, smx[w]);
+            }
+            tmin[t] = e > b ? mn : 0;
+            // overflow-safe span (times are arbitrary int64 ticks)
+            const uint64_t sp = (uint64_t)mx - (uint64_t)mn;
+            tspan[t] = e > b ? (sp > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)sp) : 0;
+        }
+    }
     int64_t g = 0;
     for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) g = gcd64(size[i], g);
     for (int o = 16; o; o >>= 1) g = gcd64(g, __shfl_xor_sync(0xFFFFFFFFu, g, o));
@@ -226,8 +256,10 @@ __global__ void k_pack(const uint32_t *__restrict__ tix, const int64_t *__restri
                        const uint32_t *__restrict__ arank, const uint32_t *__restrict__ frank,
                        const uint32_t *__restrict__ posof, const uint32_t *__restrict__ prio,
                        const uint32_t *__restrict__ sar, const int64_t *__restrict__ size,
-                       const int64_t *__restrict__ unit,
-                       int64_t N, uint2 *__restrict__ ent, Rec *__restrict__ rec) {
+                       const int64_t *__restrict__ unit, const int64_t *__restrict__ alloc,
+                       const int64_t *__restrict__ free_, const int64_t *__restrict__ tmin,
+                       int64_t N, uint2 *__restrict__ ent, Rec *__restrict__ rec,
+                       uint2 *__restrict__ raw2, uint32_t *__restrict__ rawpos) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
          k += (int64_t)gridDim.x * blockDim.x) {
         uint32_t t = tix[k];
@@ -244,15 +276,20 @@ __global__ void k_pack(const uint32_t *__restrict__ tix, const int64_t *__restri
         r.size = size[k] / unit[t];  // in units of the trace's size gcd
         rec[b + prio[k]] = r;
         ent[b + r.pos] = make_uint2(r.frank, prio[k]);
+        // raw times relative to the trace origin (meaningful when span < 2^31)
+        const uint32_t ra = (uint32_t)(alloc[k] - tmin[t]), rf = (uint32_t)(free_[k] - tmin[t]);
+        raw2[b + prio[k]] = make_uint2(ra, rf);
+        rawpos[b + r.pos] = ra;
     }
 }
 
 // One warp per chunk: bitonic-sort the chunk's 32 (free rank, slot) keys,
-// emit SF/SP/PM and the chunk summary.
+// emit SF/SP, the chunk skeleton and the live count.
 __global__ void k_chunk_sort(const int64_t *__restrict__ trace_ptr, int64_t T,
                              const uint2 *__restrict__ ent, uint32_t *__restrict__ sf,
-                             uint32_t *__restrict__ sp, uint32_t *__restrict__ pm,
-                             uint4 *__restrict__ summ, int64_t nchunks) {
+                             uint32_t *__restrict__ sp, uint4 *__restrict__ s0,
+                             uint4 *__restrict__ s1, uint32_t *__restrict__ s2,
+                             uint32_t *__restrict__ cnt, int64_t nchunks) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -265,13 +302,14 @@ __global__ void k_chunk_sort(const int64_t *__restrict__ trace_ptr, int64_t T,
         }
         const int64_t t = lo, b = trace_ptr[t], n = trace_ptr[t + 1] - b;
         const int64_t j = cg - chunk_base(b, t);
-        if (j >= ((n + 31) >> 5)) continue;  // gap between traces
-        const int64_t p = 32 * j + lane;
         uint32_t key = 0xFFFFFFFFu, pr = kDead;
-        if (p < n) {
-            const uint2 e = ent[b + p];
-            key = (e.x << 5) | (uint32_t)lane;
-            pr = e.y;
+        if (j < ((n + 31) >> 5)) {  // else: gap chunk between traces (never read)
+            const int64_t p = 32 * j + lane;
+            if (p < n) {
+                const uint2 e = ent[b + p];
+                key = (e.x << 5) | (uint32_t)lane;
+                pr = e.y;
+            }
         }
         // bitonic sort ascending by key across the warp (payload pr)
 #pragma unroll
@@ -286,21 +324,36 @@ __global__ void k_chunk_sort(const int64_t *__restrict__ trace_ptr, int64_t T,
                 if (take) { key = ok; pr = op; }
             }
         }
-        uint32_t m = pr;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, m, o);
-            if (lane >= o) m = min(m, v);
-        }
         sf[32 * cg + lane] = key;
         sp[32 * cg + lane] = pr;
-        pm[32 * cg + lane] = m;
-        const unsigned live = __ballot_sync(0xFFFFFFFFu, pr != kDead);
-        const uint32_t fr = key >> 5;
-        const uint32_t mn = live ? __shfl_sync(0xFFFFFFFFu, fr, __ffs(live) - 1) : 0xFFFFFFFFu;
-        const uint32_t mx = live ? __shfl_sync(0xFFFFFFFFu, fr, 31 - __clz(live)) : 0u;
-        const uint32_t bp = __shfl_sync(0xFFFFFFFFu, m, 31);
-        if (lane == 0) summ[cg] = make_uint4(mn, mx, bp, (uint32_t)__popc(live));
+        const uint32_t nlive = skel_store(key, pr, lane, s0, s1, s2, cg);
+        if (lane == 0) cnt[cg] = nlive;
+    }
+}
+
+// One warp per group of 32 chunks: the group skeleton (plan_types.cuh).
+__global__ void k_group_skel(const int64_t *__restrict__ trace_ptr, int64_t T,
+                             const uint4 *__restrict__ s0, const uint32_t *__restrict__ rawpos,
+                             uint4 *__restrict__ gs, int64_t ngroups) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t gg = warp; gg < ngroups; gg += nw) {
+        int64_t lo = 0, hi = T;  // owning trace: last t with group_base <= gg
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (group_base(trace_ptr[mid], mid) <= gg) lo = mid; else hi = mid;
+        }
+        const int64_t t = lo, b = trace_ptr[t], n = trace_ptr[t + 1] - b;
+        const int64_t nch = (n + 31) >> 5, g = gg - group_base(b, t);
+        if (g >= ((nch + 31) >> 5)) {  // gap group between traces (never read)
+            if (lane == 0) gs[gg] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u);
+            continue;
+        }
+        group_store(s0 + chunk_base(b, t), nch, gs + group_base(b, t), g, lane);
+        __syncwarp();
+        // GS.w: relative raw alloc time of the group's first position
+        if (lane == 0) gs[gg].w = rawpos[b + 1024 * g];
     }
 }
 
@@ -451,17 +504,23 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
     k_inverse<<<g1, kThreads, 0, s>>>(pord, tix, in.trace_ptr, N, prio);
     g_prep_k++;
 
-    k_trace_scale<<<(unsigned)T, kThreads, 0, s>>>(in.trace_ptr, in.size, out.unit,
-                                                  out.total_units);
+    k_trace_scale<<<(unsigned)T, kThreads, 0, s>>>(in.trace_ptr, in.size, in.alloc, in.free_,
+                                                  out.unit, out.total_units, out.tmin,
+                                                  out.tspan);
     g_prep_k++;
     k_pack<<<g1, kThreads, 0, s>>>(tix, in.trace_ptr, arank, frank, posof, prio, sar, in.size,
-                                   out.unit, N, out.ent, out.rec);
+                                   out.unit, in.alloc, in.free_, out.tmin, N, out.ent, out.rec,
+                                   out.raw2, out.rawpos);
     g_prep_k++;
     if (out.sf) {
-        const int64_t chunks = N / 32 + T + 1;
+        const int64_t chunks = out.nchunks;
         const int blocks = (int)std::min<int64_t>((chunks + 7) / 8, 148 * 64);
-        k_chunk_sort<<<blocks, 256, 0, s>>>(in.trace_ptr, T, out.ent, out.sf, out.sp, out.pm,
-                                            out.summ, chunks);
+        k_chunk_sort<<<blocks, 256, 0, s>>>(in.trace_ptr, T, out.ent, out.sf, out.sp, out.s0,
+                                            out.s1, out.s2, out.cnt, chunks);
+        g_prep_k++;
+        const int gblocks = (int)std::min<int64_t>((out.ngroups + 7) / 8, 148 * 64);
+        k_group_skel<<<gblocks, 256, 0, s>>>(in.trace_ptr, T, out.s0, out.rawpos, out.gs,
+                                             out.ngroups);
         g_prep_k++;
     }
     MP_CUDA(cudaGetLastError());

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+for cfg in "MEMPLAN_NWARPS=8" "MEMPLAN_NWARPS=1" "MEMPLAN_NWARPS=1 MEMPLAN_TIER=0" "MEMPLAN_NWARPS=8 MEMPLAN_TIER=0"; do
+  echo "== $cfg"
+  env $cfg timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-check ${BENCH_ARGS} 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value']/1e6, 'Mblocks/s', d['ms_per_step'], 'ms', 'single', d['single_trace']['latency_ms'], 'engine', d['plan_info']['engine'])"
+done
