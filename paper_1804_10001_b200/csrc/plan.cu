@@ -57,8 +57,9 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kPendCap = 256;  // pending segment slots per warp (shared memory)
 
-// Shared-memory tiers for the window structures.
-enum { TIER_GLOBAL = 0, TIER_SKEL = 1, TIER_ALL = 2 };
+// Shared-memory tiers for the window structures: nothing / group skeleton /
+// + chunk skeleton / + chunk-sorted table.
+enum { TIER_GLOBAL = 0, TIER_GROUP = 1, TIER_SKEL = 2, TIER_ALL = 3 };
 
 struct PlanArgs {
     const int64_t *trace_ptr;
@@ -145,6 +146,7 @@ struct Win {
 struct RetireRow {
     uint32_t key, pr;
     int j;
+    uint4 gq;  // S0 of chunk 32*(j>>5) + lane (the retired chunk's group)
 };
 
 __device__ __forceinline__ RetireRow retire_load(const Win &w, uint32_t pos, int lane) {
@@ -152,6 +154,9 @@ __device__ __forceinline__ RetireRow retire_load(const Win &w, uint32_t pos, int
     r.j = (int)(pos >> 5);
     r.key = w.sf[32 * r.j + lane];
     r.pr = w.sp[32 * r.j + lane];
+    const int jj = (r.j & ~31) + lane;
+    r.gq = make_uint4(kNone, kNone, kNone, 0u);
+    if (jj < w.nch) r.gq = w.s0[jj];
     return r;
 }
 
@@ -163,10 +168,12 @@ __device__ __forceinline__ void retire_finish(const Win &w, RetireRow r, uint32_
         r.pr = kDead;
         w.sp[32 * r.j + lane] = kDead;
     }
-    const uint32_t nlive = skel_store(r.key, r.pr, lane, w.s0, w.s1, w.s2, r.j);
+    uint4 q;
+    const uint32_t nlive = skel_store(r.key, r.pr, lane, w.s0, w.s1, w.s2, r.j, &q);
     if (STATS && lane == 0) w.cnt[r.j] = nlive;
-    __syncwarp();
-    group_store(w.s0, w.nch, w.gs, r.j >> 5, lane);
+    // the group's other chunks are unchanged: patch in the new S0 and reduce
+    if (lane == (r.j & 31)) r.gq = q;
+    group_reduce(r.gq, w.gs, r.j >> 5, lane);
 }
 
 // Step state shared between the leader warp and the query warps (NW > 1).
@@ -242,18 +249,20 @@ __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint
     bool need = false;
     uint32_t code = 0, pe = kNone;
     if (valid) {
+        // all three skeleton records at once: one memory round
         const uint4 q = w.s0[j];  // {K0, A, P, K15}
+        const uint4 r = w.s1[j];  // {K7, K23, P7, P15}
+        const uint32_t p23 = w.s2[j];
         if (q.x <= thr) {
             if (q.y <= thr) {
                 best = min(best, q.z);  // the chunk's best live entry fits
             } else {
                 // the fitting prefix ends inside segment s; pb / pe = prefix
                 // minima before / through segment s
-                const uint4 r = w.s1[j];  // {K7, K23, P7, P15}
                 uint32_t pb, s;
                 if (q.w <= thr) {
-                    if (r.y <= thr) { s = 3; pb = w.s2[j]; pe = q.z; }
-                    else { s = 2; pb = r.w; pe = w.s2[j]; }
+                    if (r.y <= thr) { s = 3; pb = p23; pe = q.z; }
+                    else { s = 2; pb = r.w; pe = p23; }
                 } else {
                     if (r.x <= thr) { s = 1; pb = r.z; pe = r.w; }
                     else { s = 0; pb = kNone; pe = r.z; }
@@ -293,7 +302,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
     // left edge chunk (warp 0): issue the row read now, consume at the end
     bool edge = false;
     uint32_t ek = kNone, ep = kDead;
-    if (warp == 0 && partial && w.s0[c0].x <= thr) {
+    if (warp == 0 && partial) {  // speculative: no dependent skeleton check first
         edge = true;
         ek = w.sf[32 * c0 + lane];
         ep = w.sp[32 * c0 + lane];
@@ -440,7 +449,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     win.nch = nch;
     const int ngr = (nch + 31) >> 5;
     const int64_t gbase = group_base(base, t);
-    if (TIER >= TIER_SKEL) {
+    if (TIER >= TIER_GROUP) {
         uint4 *g = reinterpret_cast<uint4 *>(smem + off);
         off += (size_t)ngr * 16;
         for (int i = threadIdx.x; i < ngr; i += 32 * NW) g[i] = a.gs[gbase + i];
@@ -781,6 +790,7 @@ int launch_tier(const PlanArgs &a, int grid, int tier, size_t smem, cudaStream_t
     switch (tier) {
         case TIER_ALL: return launch_nw<HT, Ls, ST, TIER_ALL>(a, grid, smem, s);
         case TIER_SKEL: return launch_nw<HT, Ls, ST, TIER_SKEL>(a, grid, smem, s);
+        case TIER_GROUP: return launch_nw<HT, Ls, ST, TIER_GROUP>(a, grid, smem, s);
         default: return launch_nw<HT, Ls, ST, TIER_GLOBAL>(a, grid, smem, s);
     }
 }
@@ -832,19 +842,24 @@ Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwar
     const size_t lines_b = lines_bytes(lcap, hbytes);
     const size_t pend_b = (size_t)nwarps * 2 * kPendCap * sizeof(uint32_t);
     const int64_t nch = (nmax + 31) / 32;
-    const size_t skel_b = (size_t)nch * 32 + a16((size_t)nch * 4) + (size_t)((nch + 31) / 32) * 16;
+    const size_t grp_b = (size_t)((nch + 31) / 32) * 16;
+    const size_t skel_b = (size_t)nch * 32 + a16((size_t)nch * 4);
     const size_t tab_b = (size_t)nch * 32 * 8;
     const size_t rec_b = (size_t)nmax * 32;
     size_t used = pend_b;
     if (!force_global) {
         if (!lines_global && used + lines_b <= lim) { l.lines_smem = true; used += lines_b; }
-        if (used + skel_b <= lim) {
-            l.tier = TIER_SKEL;
-            used += skel_b;
-            if (used + tab_b <= lim) {
-                l.tier = TIER_ALL;
-                used += tab_b;
-                if (used + rec_b <= lim) { l.rec_smem = true; used += rec_b; }
+        if (used + grp_b <= lim) {
+            l.tier = TIER_GROUP;
+            used += grp_b;
+            if (used + skel_b <= lim) {
+                l.tier = TIER_SKEL;
+                used += skel_b;
+                if (used + tab_b <= lim) {
+                    l.tier = TIER_ALL;
+                    used += tab_b;
+                    if (used + rec_b <= lim) { l.rec_smem = true; used += rec_b; }
+                }
             }
         }
     }
@@ -955,10 +970,11 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
         const int v = atoi(env);
         if (v >= TIER_GLOBAL && v < lay.tier) {
             lay = choose_layout(nmax, lcap_s, hb, budget, g_nwarps, force_global);
-            if (v == TIER_GLOBAL) {
-                lay.tier = TIER_GLOBAL;
+            if (v <= TIER_GROUP) {
+                lay.tier = v;
                 lay.rec_smem = false;
-                lay.smem = lines_bytes(lcap_s, hb) + (size_t)g_nwarps * 2 * kPendCap * 4;
+                lay.smem = lines_bytes(lcap_s, hb) + (size_t)g_nwarps * 2 * kPendCap * 4 +
+                           (v == TIER_GROUP ? (size_t)((nmax + 1023) / 1024) * 16 : 0);
             }
         }
     }
@@ -1049,7 +1065,7 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     g_info.launches = prep_launches() + (g_launches - launches0);
     g_info.engine = (h32 ? 16 : 0) | (lay.lines_smem ? 8 : 0) | (lay.tier >= TIER_SKEL ? 4 : 0) |
                     (lay.tier == TIER_ALL ? 2 : 0) | (lay.rec_smem ? 1 : 0) |
-                    (redo.empty() ? 0 : 32);
+                    (redo.empty() ? 0 : 32) | (lay.tier >= TIER_GROUP ? 64 : 0);
     g_info.cluster = g_nwarps;  // warps per trace (single-CTA engine)
     for (int64_t t = 0; t < T; t++) {
         g_info.steps += hst[t * ST_N + ST_STEPS];

@@ -68,15 +68,11 @@ __host__ __device__ inline int64_t group_base(int64_t trace_base, int64_t t) {
 }
 
 #ifdef __CUDACC__
-// Rebuild and store group g's skeleton from its chunks' S0 (one warp; lane =
-// chunk within the group; chunks at or beyond nch count as empty).
-__device__ __forceinline__ void group_store(const uint4 *s0, int64_t nch, uint4 *gs, int64_t g,
-                                            int lane) {
+// Group skeleton of group g from its chunks' S0 (one warp; lane = chunk
+// within the group, q = that chunk's S0 or all-ones past the trace end).
+__device__ __forceinline__ void group_reduce(uint4 q, uint4 *gs, int64_t g, int lane) {
     constexpr unsigned full = 0xFFFFFFFFu;
     constexpr uint32_t none = 0xFFFFFFFFu;
-    const int64_t j = 32 * g + lane;
-    uint4 q = make_uint4(none, none, none, 0);
-    if (j < nch) q = s0[j];
     const uint32_t g0 = __reduce_min_sync(full, q.x);
     const uint32_t gp = __reduce_min_sync(full, q.z);
     const unsigned at = __ballot_sync(full, q.z == gp && gp != none);
@@ -89,11 +85,20 @@ __device__ __forceinline__ void group_store(const uint4 *s0, int64_t nch, uint4 
     }
 }
 
+__device__ __forceinline__ void group_store(const uint4 *s0, int64_t nch, uint4 *gs, int64_t g,
+                                            int lane) {
+    const int64_t j = 32 * g + lane;
+    uint4 q = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u);
+    if (j < nch) q = s0[j];
+    group_reduce(q, gs, g, lane);
+}
+
 // Rebuild and store the skeleton of chunk j from its sorted row (one warp;
 // lane = sorted slot, `key` = SF, `pr` = SP with retired / padding slots at
 // kDead).  Returns the live count.
 __device__ __forceinline__ uint32_t skel_store(uint32_t key, uint32_t pr, int lane, uint4 *s0,
-                                               uint4 *s1, uint32_t *s2, int64_t j) {
+                                               uint4 *s1, uint32_t *s2, int64_t j,
+                                               uint4 *s0_out = nullptr) {
     constexpr unsigned full = 0xFFFFFFFFu;
     constexpr uint32_t none = 0xFFFFFFFFu;
     const unsigned live = __ballot_sync(full, pr != kDead);
@@ -111,6 +116,7 @@ __device__ __forceinline__ uint32_t skel_store(uint32_t key, uint32_t pr, int la
         s1[j] = make_uint4(k7, k23, p7, p15);
         s2[j] = p23;
     }
+    if (s0_out) *s0_out = make_uint4(k0, a, p, k15);
     return (uint32_t)__popc(live);
 }
 #endif
