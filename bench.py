@@ -306,6 +306,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "sample": f"{procs} traces x {args.n} blocks, one per process "
                              f"({r['per_trace_s']:.1f} s/trace; oracle/bestfit_np.py numpy "
                              f"restatement of memplan.bestfit)"}
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                rec = json.load(fh).get(f"uniform n={args.n} traces={args.traces}")
+            traffic = int(rec["dram_bytes"]) if rec else None
+        except (OSError, ValueError, KeyError):
+            traffic = None
+        steps_per_trace = info_stats["steps"] / T
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -316,11 +324,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                     "d2h_bytes_per_step": int(8 * (NB + T))},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_kind,
-                         "kernel": "k_plan_sorted (K1 planner)",
-                         "bytes_def": "B_alg = 24*sum(W_live) + 32*n per trace (SURVEY §8(d))",
-                         "alg_bytes_per_launch": b_alg, "kernel_ms": kms},
+                         "kernel": "k_plan (K1/K2 planner, batched launch)",
+                         "bytes_def": "B_alg = 24*sum(W_live) + 32*n per trace (SURVEY §8(d)); "
+                                      "the kernel answers most window entries from chunk/group "
+                                      "skeletons, so B_alg/t exceeds the HBM peak (DESIGN.md §5)",
+                         "alg_bytes_per_launch": b_alg, "kernel_ms": kms,
+                         "traffic_frac": (traffic / (kms / 1e3) / 1e9 / peak) if traffic else None,
+                         "latency": {"steps_per_trace": steps_per_trace,
+                                     "ns_per_step_per_trace": kms * 1e6 / steps_per_trace,
+                                     "traces_resident_per_sm": args.traces / 148.0}},
             "cpu_baseline": cpu,
             "clocks": clk,
             "single_trace": {"n": args.n, "latency_ms": lat_ms,

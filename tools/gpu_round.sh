@@ -18,5 +18,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_plan -s 2 -c 1 \
   -o gpurun_out/prof_${TAG} python bench.py --steps 1 --warmup 3 --no-cpu --no-check \
   ${BENCH_ARGS} > gpurun_out/prof_${TAG}.log 2>&1
-tail -3 gpurun_out/pytest_gpu_${TAG}.log gpurun_out/smoke_${TAG}.log gpurun_out/bench_${TAG}.log \
+tail -n 3 gpurun_out/pytest_gpu_${TAG}.log gpurun_out/smoke_${TAG}.log gpurun_out/bench_${TAG}.log \
   gpurun_out/prof_${TAG}.log
