@@ -166,6 +166,86 @@ def run_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def _best_wall(fn, reps):
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = fn()
+        best = min(best, time.perf_counter() - t0)
+    return best, r
+
+
+def _lstm_cpu_one(traces):
+    from oracle.bestfit_np import solve_bestfit_np
+    for a, f, s in traces:
+        solve_bestfit_np(a, f, s)
+    return len(traces)
+
+
+def config_suite(cpu_procs: int) -> dict:
+    """BASELINE.json configs[0..3] (+ single-trace synthetic latency): plan
+    latency host-to-host and device-side on the GPU, the CPU port beside it,
+    bit-exact against the C oracle.  Small, bounded (tens of seconds)."""
+    import oracle
+    import paper_1804_10001_b200 as mp
+    from paper_1804_10001_b200.bestfit import (solve_bestfit_arrays, plan_info,
+                                               solve_bestfit_batched_arrays)
+    from oracle.bestfit_np import solve_bestfit_np
+    out = {}
+    cases = [("alexnet_mb32", "alexnet", 32), ("googlenet_mb64", "googlenet", 64),
+             ("resnet50_mb64", "resnet50", 64), ("inception_resnet_v2_mb128",
+                                                 "inception_resnet_v2", 128)]
+    insts = [(k, mp.profile_to_instance(mp.record(mp.parse_trace(mp.net_trace(net, b))),
+                                        alignment=ALIGN).arrays()) for k, net, b in cases]
+    for name, n in (("cnn_1e4", 10000), ("uniform_1e4", 10000)):
+        if name.startswith("cnn"):
+            arr = mp.profile_to_instance(mp.record(mp.parse_trace(mp.cnn_like_trace(
+                mp.GenSpec(model="cnn", layers=n // 2, seed=0)))), alignment=ALIGN).arrays()
+        else:
+            from paper_1804_10001_b200.workloads import uniform_arrays
+            a, f, s = uniform_arrays(n, 0)
+            arr = (a, f, ((s + ALIGN - 1) // ALIGN) * ALIGN)
+        insts.append((name, arr))
+    for key, (a, f, s) in insts:
+        solve_bestfit_arrays(a, f, s)  # warm-up (module load, pools)
+        wall, (off, pk) = _best_wall(lambda: solve_bestfit_arrays(a, f, s), 5)
+        info = plan_info()
+        ref_off, ref_pk = oracle.solve_bestfit(a, f, s)
+        cpu_wall, _ = _best_wall(lambda: solve_bestfit_np(a, f, s), 3 if len(a) < 5000 else 1)
+        out[key] = {"blocks": int(len(a)), "peak_bytes": int(pk),
+                    "gpu_host_to_host_ms": 1e3 * wall,
+                    "gpu_device_ms": float(info["prep_ms"] + info["plan_ms"]),
+                    "cpu_port_1core_ms": 1e3 * cpu_wall,
+                    "speedup_vs_1core": cpu_wall / wall,
+                    "bit_exact_vs_oracle": bool(np.array_equal(off, ref_off) and pk == ref_pk)}
+    # configs[3]: 4096 variable-length LSTM seq2seq profiles planned batched
+    from paper_1804_10001_b200.workloads import lstm_profiles
+    profs = lstm_profiles(4096, layers=6, batch=64)
+    arrs = [mp.profile_to_instance(mp.record(mp.parse_trace(t)), alignment=ALIGN).arrays()
+            for t in profs]
+    tp = np.zeros(len(arrs) + 1, np.int64)
+    np.cumsum([len(x[0]) for x in arrs], out=tp[1:])
+    A = np.concatenate([x[0] for x in arrs]); F = np.concatenate([x[1] for x in arrs])
+    S = np.concatenate([x[2] for x in arrs])
+    solve_bestfit_batched_arrays(tp, A, F, S)
+    wall, (off, pks) = _best_wall(lambda: solve_bestfit_batched_arrays(tp, A, F, S), 5)
+    info = plan_info()
+    exact = all(int(pks[t]) == oracle.solve_bestfit(*arrs[t])[1] for t in range(0, 4096, 97))
+    import multiprocessing as mpc
+    chunks = [arrs[i::cpu_procs] for i in range(cpu_procs)]
+    with mpc.get_context("fork").Pool(cpu_procs) as pool:
+        pool.map(_lstm_cpu_one, [c[:4] for c in chunks])
+        t0 = time.perf_counter()
+        pool.map(_lstm_cpu_one, chunks)
+        cpu_wall = time.perf_counter() - t0
+    out["lstm_4096_profiles_L6_b64"] = {
+        "blocks": int(len(A)), "traces": 4096, "gpu_host_to_host_ms": 1e3 * wall,
+        "gpu_device_ms": float(info["prep_ms"] + info["plan_ms"]),
+        "cpu_port_ms": 1e3 * cpu_wall, "cpu_cores": cpu_procs,
+        "speedup_vs_cpu": cpu_wall / wall, "peaks_exact_sampled_vs_oracle": bool(exact)}
+    return out
+
+
 def bench_config(args, world):
     return {"workload": f"uniform random-lifetime traces, n={args.n} blocks each, "
                         f"{args.traces} traces per GPU per step (BASELINE.json configs[4])",
@@ -314,6 +394,34 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         except (OSError, ValueError, KeyError):
             traffic = None
         steps_per_trace = info_stats["steps"] / T
+        suite = None
+        if world == 1 and not args.no_suite:
+            try:
+                suite = config_suite(min(host_cores(), args.cpu_procs))
+            except Exception as exc:  # noqa: BLE001  (reported, not fatal)
+                suite = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        replay = None
+        if world == 1 and not args.no_replay:
+            try:
+                r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "replay_bench.py"),
+                                    "--alloc", "all", "--reps", "10"], capture_output=True,
+                                   text=True, timeout=600)
+                rl = [x for x in r.stdout.splitlines() if x.startswith("{")]
+                rr = json.loads(rl[-1]) if rl else {}
+                replay = {"unit": "ns/alloc",
+                          "trace": "cnn-like L=5000 (10^4 allocs/epoch), best of 10 epochs",
+                          "memplan_c_abi_arena": rr.get("carena", {}).get("ns_per_alloc"),
+                          "memplan_torch_hooks": rr.get("memplan", {}).get("hook_ns_per_alloc"),
+                          "memplan_via_torch_pluggable":
+                              rr.get("memplan", {}).get("ns_per_alloc"),
+                          "torch_caching_allocator": rr.get("caching", {}).get("ns_per_alloc"),
+                          "torch_cudaMallocAsync": rr.get("async", {}).get("ns_per_alloc"),
+                          "addresses_match_plan":
+                              rr.get("memplan", {}).get("addresses_match_plan"),
+                          "plan_peak_bytes": rr.get("memplan", {}).get("plan_peak_bytes"),
+                          "pool_peak_bytes": rr.get("memplan", {}).get("pool_peak_bytes")}
+            except (OSError, ValueError, subprocess.SubprocessError) as exc:
+                replay = {"error": str(exc)[:200]}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -343,6 +451,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "plan_info": {k: info_stats[k] for k in ("steps", "lifts", "max_lines", "engine",
                                                      "sum_wlive")},
             "parity_trace0_vs_oracle": parity,
+            "replay": replay,
+            "configs": suite,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -360,6 +470,8 @@ def main():
     p.add_argument("--traces", type=int, default=1184)
     p.add_argument("--cpu-procs", type=int, default=32)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-replay", action="store_true")
+    p.add_argument("--no-suite", action="store_true")
     p.add_argument("--check", action="store_true", default=True)
     p.add_argument("--no-check", dest="check", action="store_false")
     args = p.parse_args()

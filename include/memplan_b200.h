@@ -189,6 +189,17 @@ int mp_torch_set_mode(int mode, mp_arena *arena);
 /* Recorded trace since the last mode switch: kind 0 alloc(size), 1 free(ref). */
 int mp_torch_get_trace(int32_t *kinds, int64_t *values, int64_t cap, int64_t *n_out);
 int mp_torch_epoch_reset(void); /* start a new replay epoch (Arena.reset) */
+/* Replay through torch over ONE cudaMalloc'd region of plan.peak bytes:
+ * allocates the region (outside torch's allocator, so torch never sees its
+ * base pointer as an allocation of its own), rebases `arena` onto it and
+ * switches the hooks to replay mode.  _end switches back to passthrough and
+ * frees the region. */
+int mp_torch_replay_begin(mp_arena *arena, int device, uint64_t *base_out);
+int mp_torch_replay_end(void);
+/* Benchmark helper: replay the epoch `reps` times through mp_torch_alloc /
+ * mp_torch_free directly (replay mode), best mean host ns per alloc call. */
+int mp_torch_bench(const int32_t *kinds, const int64_t *values, int64_t n_events, int64_t reps,
+                   double *ns_per_alloc);
 
 /* ---- fallback pool (arena.py:59-129 PoolAllocator / :343-364) ------------ */
 typedef struct mp_pool mp_pool;

@@ -102,6 +102,10 @@ SIGNATURES = [
     ("mp_torch_set_mode", ctypes.c_int, [ctypes.c_int, VP]),
     ("mp_torch_get_trace", ctypes.c_int, [VP, VP, ctypes.c_int64, P64]),
     ("mp_torch_epoch_reset", ctypes.c_int, []),
+    ("mp_torch_replay_begin", ctypes.c_int, [VP, ctypes.c_int, PU64]),
+    ("mp_torch_replay_end", ctypes.c_int, []),
+    ("mp_torch_bench", ctypes.c_int, [VP, VP, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.POINTER(ctypes.c_double)]),
     ("mp_pool_create", ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(VP)]),
     ("mp_pool_destroy", None, [VP]),
     ("mp_pool_alloc", ctypes.c_int, [VP, ctypes.c_int64, P64, P64]),

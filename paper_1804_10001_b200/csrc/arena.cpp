@@ -12,6 +12,7 @@
 // Pool replaces PoolAllocator (arena.py:59-129): smallest sufficient free
 // block reused whole (ties: lowest address), else bump allocation; finite
 // capacity flushes the pool before failing.
+#include <algorithm>
 #include <chrono>
 #include <mutex>
 #include <set>
@@ -491,6 +492,12 @@ struct TorchState {
     // replay mode: pointers served outside the plan (growth/extra/interrupt)
     std::unordered_map<uintptr_t, int64_t> side;     // ptr -> ref
     int64_t n_allocs = 0;
+    void *region = nullptr;  // the one cudaMalloc'd replay region (mp_torch_replay_begin)
+    int device = 0;          // device of the replay arena
+    // live planned blocks by address: slot (addr - base) >> gshift -> ref
+    std::vector<int64_t> slot_ref;
+    uint64_t span = 0, gran = 1;
+    int gshift = 0;
 };
 
 TorchState &ts() {
@@ -501,6 +508,43 @@ TorchState &ts() {
 }  // namespace
 
 extern "C" {
+
+int mp_torch_replay_begin(mp_arena *arena, int device, uint64_t *base_out) {
+    TorchState &s = ts();
+    if (!arena) {
+        set_error("null arena");
+        return MP_ERR_INVALID;
+    }
+    {
+        std::lock_guard<std::mutex> g(s.mu);
+        if (s.region) {
+            set_error("a replay region is already active");
+            return MP_ERR_INVALID;
+        }
+    }
+    MP_TRY(mp::use_device(device));
+    void *p = nullptr;
+    const size_t bytes = arena->plan_peak > 0 ? (size_t)arena->plan_peak : 1;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return mp::cuda_fail(e, "cudaMalloc(replay region)");
+    arena->base = (uint64_t)(uintptr_t)p;
+    MP_TRY(mp_torch_set_mode(2, arena));
+    std::lock_guard<std::mutex> g(s.mu);
+    s.region = p;
+    if (base_out) *base_out = arena->base;
+    return MP_OK;
+}
+
+int mp_torch_replay_end(void) {
+    TorchState &s = ts();
+    MP_TRY(mp_torch_set_mode(0, nullptr));
+    std::lock_guard<std::mutex> g(s.mu);
+    if (s.region) {
+        cudaFree(s.region);
+        s.region = nullptr;
+    }
+    return MP_OK;
+}
 
 int mp_torch_set_mode(int mode, mp_arena *arena) {
     TorchState &s = ts();
@@ -514,7 +558,26 @@ int mp_torch_set_mode(int mode, mp_arena *arena) {
     s.kinds.clear();
     s.values.clear();
     s.ptr_ref.clear();
+    s.slot_ref.clear();
     s.n_allocs = 0;
+    if (mode == 2) {
+        // planned addresses are base + (multiples of the alignment): index the
+        // live blocks directly when the table stays small
+        uint64_t g = 1;
+        int sh = 0;
+        while ((int64_t)(g << 1) <= arena->alignment && (arena->alignment % (int64_t)(g << 1)) == 0) {
+            g <<= 1;
+            sh++;
+        }
+        const uint64_t span = arena->plan_peak > 0 ? (uint64_t)arena->plan_peak : 0;
+        if (span / g <= (uint64_t(1) << 24)) {
+            s.gran = g;
+            s.gshift = sh;
+            s.span = span;
+            s.slot_ref.assign((size_t)(span / g) + 1, 0);
+        }
+        cudaGetDevice(&s.device);
+    }
     return MP_OK;
 }
 
@@ -535,6 +598,7 @@ int mp_torch_epoch_reset(void) {
     std::lock_guard<std::mutex> g(s.mu);
     s.n_allocs = 0;
     s.ptr_ref.clear();
+    std::fill(s.slot_ref.begin(), s.slot_ref.end(), 0);
     if (s.mode == 2 && s.arena) return s.arena->reset();
     return MP_OK;
 }
@@ -543,30 +607,40 @@ void *mp_torch_alloc(size_t size, int device, mp_stream_t stream) {
     (void)stream;
     TorchState &s = ts();
     std::lock_guard<std::mutex> g(s.mu);
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (cur != device) cudaSetDevice(device);
     if (s.mode == 2 && s.arena) {
         mp_arena *a = s.arena;
         const int64_t bid = a->lam;
         const int64_t sz = (int64_t)size;
-        if (a->depth == 0 && !a->closed && bid <= a->nblocks() && sz <= a->expected[bid] && sz > 0) {
+        if (device == s.device && a->depth == 0 && !a->closed && bid <= a->nblocks() &&
+            sz <= a->expected[bid] && sz > 0) {
+            // hot path: base + offset[lambda] and one table store for the free
             uint64_t addr = 0;
             if (a->alloc(sz, &addr) == MP_OK) {
                 s.n_allocs++;
-                s.ptr_ref[(uintptr_t)addr] = (int64_t)a->seq.size();
+                const int64_t ref = (int64_t)a->seq.size();
+                const uint64_t rel = addr - a->base;
+                if (!s.slot_ref.empty() && rel < s.span && (rel & (s.gran - 1)) == 0)
+                    s.slot_ref[rel >> s.gshift] = ref;
+                else
+                    s.ptr_ref[(uintptr_t)addr] = ref;
                 return (void *)addr;
             }
         }
         // outside the plan: live tensors cannot move, so serve from a side
         // allocation and remember the observed size for the next re-plan
         if (a->depth == 0 && bid <= a->nblocks() && sz > a->observed[bid]) a->observed[bid] = sz;
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != device) cudaSetDevice(device);
         void *p = nullptr;
         if (cudaMalloc(&p, size ? size : 1) != cudaSuccess) return nullptr;
         s.side[(uintptr_t)p] = ++s.n_allocs;
         if (a->depth == 0) a->lam++;
         return p;
     }
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != device) cudaSetDevice(device);
     void *p = nullptr;
     if (cudaMalloc(&p, size ? size : 1) != cudaSuccess) return nullptr;
     if (s.mode == 1) {
@@ -584,18 +658,26 @@ void mp_torch_free(void *ptr, size_t size, int device, mp_stream_t stream) {
     TorchState &s = ts();
     std::lock_guard<std::mutex> g(s.mu);
     if (s.mode == 2 && s.arena) {
-        auto it = s.side.find((uintptr_t)ptr);
-        if (it != s.side.end()) {
-            s.side.erase(it);
-            cudaFree(ptr);
-            return;
+        mp_arena *a = s.arena;
+        const uint64_t rel = (uint64_t)(uintptr_t)ptr - a->base;
+        if (!s.slot_ref.empty() && rel < s.span && (rel & (s.gran - 1)) == 0) {
+            int64_t &ref = s.slot_ref[rel >> s.gshift];
+            if (ref > 0) {  // hot path: a planned block
+                a->free_ref(ref);
+                ref = 0;
+                return;
+            }
         }
         auto jt = s.ptr_ref.find((uintptr_t)ptr);
         if (jt != s.ptr_ref.end()) {
-            s.arena->free_ref(jt->second);
+            a->free_ref(jt->second);
             s.ptr_ref.erase(jt);
+            return;  // planned memory is owned by the arena region
         }
-        return;  // planned memory is owned by the arena region
+        auto it = s.side.find((uintptr_t)ptr);
+        if (it != s.side.end()) s.side.erase(it);
+        cudaFree(ptr);  // a side allocation, or a passthrough one made before replay
+        return;
     }
     if (s.mode == 1) {
         auto it = s.ptr_ref.find((uintptr_t)ptr);
@@ -606,6 +688,38 @@ void mp_torch_free(void *ptr, size_t size, int device, mp_stream_t stream) {
         }
     }
     cudaFree(ptr);
+}
+
+int mp_torch_bench(const int32_t *kinds, const int64_t *values, int64_t n_events, int64_t reps,
+                   double *ns_per_alloc) {
+    TorchState &s = ts();
+    if (s.mode != 2 || !s.arena) {
+        set_error("mp_torch_bench needs replay mode (mp_torch_replay_begin)");
+        return MP_ERR_INVALID;
+    }
+    int64_t n_alloc = 0;
+    for (int64_t i = 0; i < n_events; i++) n_alloc += kinds[i] == 0;
+    std::vector<void *> ptrs((size_t)n_alloc + 1, nullptr);
+    double best = 1e300;
+    for (int64_t r = 0; r < reps; r++) {
+        MP_TRY(mp_torch_epoch_reset());
+        int64_t k = 0;
+        auto t0 = std::chrono::steady_clock::now();
+        for (int64_t i = 0; i < n_events; i++) {
+            if (kinds[i] == 0) {
+                ptrs[k++] = mp_torch_alloc((size_t)values[i], s.device, nullptr);
+            } else if (kinds[i] == 1) {
+                mp_torch_free(ptrs[values[i] - 1], 0, s.device, nullptr);
+                ptrs[values[i] - 1] = nullptr;
+            }
+        }
+        auto t1 = std::chrono::steady_clock::now();
+        for (int64_t j = 0; j < k; j++)
+            if (ptrs[j]) mp_torch_free(ptrs[j], 0, s.device, nullptr), ptrs[j] = nullptr;
+        best = std::min(best, std::chrono::duration<double, std::nano>(t1 - t0).count());
+    }
+    *ns_per_alloc = n_alloc ? best / (double)n_alloc : 0.0;
+    return MP_OK;
 }
 
 }  // extern "C"

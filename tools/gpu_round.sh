@@ -13,10 +13,10 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 1200 python bench.py ${BENCH_ARGS} > gpurun_out/bench_${TAG}.log 2>&1
 echo "bench rc=$?" >> gpurun_out/bench_${TAG}.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-check \
+  --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-check --no-replay --no-suite \
   ${BENCH_ARGS} > gpurun_out/launches_${TAG}.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_plan -s 2 -c 1 \
-  -o gpurun_out/prof_${TAG} python bench.py --steps 1 --warmup 3 --no-cpu --no-check \
+  -o gpurun_out/prof_${TAG} python bench.py --steps 1 --warmup 3 --no-cpu --no-check --no-replay --no-suite \
   ${BENCH_ARGS} > gpurun_out/prof_${TAG}.log 2>&1
 tail -n 3 gpurun_out/pytest_gpu_${TAG}.log gpurun_out/smoke_${TAG}.log gpurun_out/bench_${TAG}.log \
   gpurun_out/prof_${TAG}.log
