@@ -98,6 +98,9 @@ template <> struct KeyT<uint32_t> {
     static __device__ __forceinline__ uint32_t h(K k) { return (uint32_t)(k >> 32); }
     static __device__ __forceinline__ uint32_t lo(K k) { return (uint32_t)k; }
     static __device__ __forceinline__ K none() { return ~0ull; }
+    static __device__ __forceinline__ uint32_t warp_min_h(uint32_t h) {
+        return __reduce_min_sync(kFull, h);
+    }
     static __device__ __forceinline__ K warp_min(K k) {
         const uint32_t a = __reduce_min_sync(kFull, (uint32_t)(k >> 32));
         const uint32_t b = __reduce_min_sync(kFull, (uint32_t)(k >> 32) == a ? (uint32_t)k
@@ -114,6 +117,12 @@ template <> struct KeyT<uint64_t> {
     static __device__ __forceinline__ uint64_t h(K k) { return (uint64_t)(k >> 32); }
     static __device__ __forceinline__ uint32_t lo(K k) { return (uint32_t)k; }
     static __device__ __forceinline__ K none() { return ~(K)0; }
+    static __device__ __forceinline__ uint64_t warp_min_h(uint64_t h) {
+        const uint32_t a = __reduce_min_sync(kFull, (uint32_t)(h >> 32));
+        const uint32_t b = __reduce_min_sync(kFull, (uint32_t)(h >> 32) == a ? (uint32_t)h
+                                                                              : 0xFFFFFFFFu);
+        return ((uint64_t)a << 32) | b;
+    }
     static __device__ __forceinline__ K warp_min(K k) {
         const uint32_t w2 = (uint32_t)(k >> 64), w1 = (uint32_t)(k >> 32), w0 = (uint32_t)k;
         const uint32_t a = __reduce_min_sync(kFull, w2);
@@ -139,7 +148,61 @@ struct Win {
     int nch;             // chunks of this trace
     uint32_t *sf, *sp;   // chunk-sorted table (shared or global)
     uint32_t *cnt;       // live count per chunk (global, STATS only)
+    uint64_t keep, stream;  // L2 policies (global tiers)
 };
+
+// L2 cache policies for the global-memory tiers: the skeletons are the hot,
+// re-read working set of every step (evict_last); records are read once per
+// placement (evict_first).
+__device__ __forceinline__ uint64_t l2_policy_keep() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_stream() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 ldg_hint(const uint4 *ptr, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(ptr), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint2 ldg_hint(const uint2 *ptr, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(ptr), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_hint(const uint32_t *ptr, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
+    return v;
+}
+// Skeleton / record loads: plain (shared memory or plain global) or with
+// the L2 policy when the structure lives in global memory.
+template <bool G, typename T> __device__ __forceinline__ T ldk(const T *p, uint64_t pol) {
+    if (G) return ldg_hint(p, pol);
+    return *p;
+}
+
+// Winner record (priority order) and its raw alloc/free.
+__device__ __forceinline__ void load_rec(const uint4 *rec4, const uint2 *raw2, uint32_t b,
+                                         bool rec_smem, uint64_t pol, uint4 &r0, uint4 &r1,
+                                         uint2 &rw) {
+    if (rec_smem) {
+        r0 = rec4[2 * b];
+        r1 = rec4[2 * b + 1];
+    } else {
+        r0 = ldg_hint(rec4 + 2 * b, pol);
+        r1 = ldg_hint(rec4 + 2 * b + 1, pol);
+    }
+    rw = ldg_hint(raw2 + b, pol);
+}
 
 // Issue the row read of the retired entry's chunk (the data is consumed by
 // retire_finish, so the latency overlaps whatever the warp does between).
@@ -149,6 +212,7 @@ struct RetireRow {
     uint4 gq;  // S0 of chunk 32*(j>>5) + lane (the retired chunk's group)
 };
 
+template <bool SG>
 __device__ __forceinline__ RetireRow retire_load(const Win &w, uint32_t pos, int lane) {
     RetireRow r;
     r.j = (int)(pos >> 5);
@@ -156,7 +220,7 @@ __device__ __forceinline__ RetireRow retire_load(const Win &w, uint32_t pos, int
     r.pr = w.sp[32 * r.j + lane];
     const int jj = (r.j & ~31) + lane;
     r.gq = make_uint4(kNone, kNone, kNone, 0u);
-    if (jj < w.nch) r.gq = w.s0[jj];
+    if (jj < w.nch) r.gq = ldk<SG>(w.s0 + jj, w.keep);
     return r;
 }
 
@@ -244,15 +308,16 @@ struct QStats {
 // fold into `best`; a straddling chunk whose boundary segment may still win
 // is appended to the warp's pending list (code = j<<2 | segment, and the
 // segment's prefix minimum as the bound it must beat).
+template <bool SG>
 __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint32_t thr,
                                            uint32_t &best, uint32_t *pend, int &np, int lane) {
     bool need = false;
     uint32_t code = 0, pe = kNone;
     if (valid) {
         // all three skeleton records at once: one memory round
-        const uint4 q = w.s0[j];  // {K0, A, P, K15}
-        const uint4 r = w.s1[j];  // {K7, K23, P7, P15}
-        const uint32_t p23 = w.s2[j];
+        const uint4 q = ldk<SG>(w.s0 + j, w.keep);  // {K0, A, P, K15}
+        const uint4 r = ldk<SG>(w.s1 + j, w.stream);  // {K7, K23, P7, P15}
+        const uint32_t p23 = ldk<SG>(w.s2 + j, w.stream);
         if (q.x <= thr) {
             if (q.y <= thr) {
                 best = min(best, q.z);  // the chunk's best live entry fits
@@ -289,12 +354,13 @@ __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint
 // Best contained block among the window chunks this warp handles (rule R4).
 // Returns the warp-wide minimum priority; `lbest` is this lane's candidate
 // and the lane holding the warp minimum has prefetched its record into r0/r1.
-template <bool STATS, int NW>
+template <bool STATS, int NW, int TIER>
 __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4, const uint2 *raw2,
                                                  uint32_t *pend, int c0, int c1, uint32_t chi,
                                                  uint32_t clop, uint32_t chip, uint32_t rawhi,
                                                  bool prune, int warp, int lane, uint32_t &lbest,
-                                                 uint4 &r0, uint4 &r1, uint2 &rw, QStats &qs) {
+                                                 uint4 &r0, uint4 &r1, uint2 &rw, QStats &qs,
+                                                 bool rec_smem) {
     const uint32_t thr = (chi << 5) | 31u;
     uint32_t best = kNone;
     const bool partial = (clop & 31u) != 0;
@@ -334,7 +400,8 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
         if (warp == 0) {
             const int j = cs + lane;
             if (STATS) qs.pass++;
-            eval_chunk(w, j, j <= c1 && j < 32 * gf, thr, best, pend, np, lane);
+            eval_chunk<(TIER < TIER_SKEL)>(w, j, j <= c1 && j < 32 * gf, thr, best, pend, np,
+                                            lane);
         }
     }
     // whole groups [gf, c1 >> 5] (none when the window is the edge chunk alone)
@@ -345,7 +412,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
         uint32_t graw = 0;
         if (STATS) qs.pass++;
         if (g <= gl) {
-            const uint4 G = w.gs[g];  // {G0, GA, GP, GR}
+            const uint4 G = ldk<(TIER < TIER_GROUP)>(w.gs + g, w.keep);  // {G0, GA, GP, GR}
             if (G.x <= thr) {
                 if (G.y <= thr) best = min(best, G.z);  // the group's best entry fits
                 else { scan = true; graw = G.w; }
@@ -360,7 +427,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
             // and id break lifetime ties).
             const uint32_t e = __reduce_min_sync(kFull, best);
             if (e != kNone) {
-                const uint2 er = raw2[e];
+                const uint2 er = ldk<true>(raw2 + e, w.stream);
                 const uint32_t lstar = er.y - er.x;
                 m = __ballot_sync(kFull, scan && rawhi - graw >= lstar);
             }
@@ -370,7 +437,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
             m &= m - 1;
             const int j = 32 * g2 + lane;
             if (STATS) qs.pass++;
-            eval_chunk(w, j, j <= c1, thr, best, pend, np, lane);
+            eval_chunk<(TIER < TIER_SKEL)>(w, j, j <= c1, thr, best, pend, np, lane);
             if (np > kPendCap - 32) {
                 if (STATS) qs.seg += np;
                 best = min(best, drain_pending(w, pend, np, thr, kNone, lane));
@@ -378,28 +445,26 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
             }
         }
     }
+    // the speculative edge row has long arrived: fold it in first
+    if (edge && (ek & 31u) >= (clop & 31u) && ek <= thr) best = min(best, ep);
     // provisional warp winner: prefetch its record while the segments load
     const uint32_t wb1 = __reduce_min_sync(kFull, best);
     if (best == wb1 && best != kNone) {
-        r0 = rec4[2 * best];
-        r1 = rec4[2 * best + 1];
-        rw = raw2[best];
+        load_rec(rec4, raw2, best, rec_smem, w.stream, r0, r1, rw);
     }
-    uint32_t b2 = kNone;
-    if (np) {
-        if (STATS) {
-            for (int e = lane; e < np; e += 32)
-                qs.seg += __popc(__ballot_sync(__activemask(), pend[kPendCap + e] < wb1));
-        }
-        b2 = drain_pending(w, pend, np, thr, wb1, lane);
+    if (!np) {
+        lbest = best;
+        return wb1;
     }
-    if (edge && (ek & 31u) >= (clop & 31u) && ek <= thr) b2 = min(b2, ep);
+    if (STATS) {
+        for (int e = lane; e < np; e += 32)
+            qs.seg += __popc(__ballot_sync(__activemask(), pend[kPendCap + e] < wb1));
+    }
+    const uint32_t b2 = drain_pending(w, pend, np, thr, wb1, lane);
     if (b2 < best) best = b2;
     const uint32_t wb = __reduce_min_sync(kFull, best);
-    if (wb != wb1 && best == wb) {  // a segment or the edge chunk improved it
-        r0 = rec4[2 * best];
-        r1 = rec4[2 * best + 1];
-        rw = raw2[best];
+    if (wb != wb1 && best == wb) {  // a pending segment improved it
+        load_rec(rec4, raw2, best, rec_smem, w.stream, r0, r1, rw);
     }
     lbest = best;
     return wb;
@@ -446,6 +511,8 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     off += (size_t)NW * 2 * kPendCap * sizeof(uint32_t);
     Win win;
     win.cnt = a.cnt + cb;
+    win.keep = l2_policy_keep();
+    win.stream = l2_policy_stream();
     win.nch = nch;
     const int ngr = (nch + 31) >> 5;
     const int64_t gbase = group_base(base, t);
@@ -534,9 +601,13 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
                 if (!known) {
                     if (STATS) nscan++;
                     if (nl <= 32) {
+                        // lane i holds line i (time order), so the leftmost
+                        // line of minimal height is the lowest lane whose
+                        // height equals the warp minimum: one reduction
                         const K k = lane < nl ? L[lane].key : KO::none();
-                        ck = KO::warp_min(k);
-                        c = __ffs(__ballot_sync(kFull, k == ck)) - 1;
+                        const HT hmin = KO::warp_min_h(KO::h(k));
+                        c = __ffs(__ballot_sync(kFull, KO::h(k) == hmin && lane < nl)) - 1;
+                        ck = KO::make(hmin, __shfl_sync(kFull, KO::lo(k), c));
                     } else {
                         K bk = KO::none();
                         int bi = 0;
@@ -581,8 +652,9 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         uint2 rw = make_uint2(0, 0);
         if (qlop < qhip) {
             const int c0 = (int)(qlop >> 5), c1 = (int)((qhip - 1) >> 5);
-            wb = query_window<STATS, NW>(win, rec4, a.raw2 + base, pend, c0, c1, qchi, qlop, qhip,
-                                         qraw, prune, warp, lane, lbest, r0, r1, rw, qs);
+            wb = query_window<STATS, NW, TIER>(win, rec4, a.raw2 + base, pend, c0, c1, qchi, qlop,
+                                               qhip, qraw, prune, warp, lane, lbest, r0, r1, rw,
+                                               qs, a.rec_smem != 0);
         }
         uint32_t gbest;
         if (NW > 1) {
@@ -601,7 +673,8 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
                 // the winning warp retires the entry while the leader
                 // rewrites the skyline (both finish before barrier [A])
                 const uint32_t pos = ss.wrec[warp][0].x;
-                retire_finish<STATS>(win, retire_load(win, pos, lane), pos, lane);
+                retire_finish<STATS>(win, retire_load<(TIER < TIER_SKEL)>(win, pos, lane), pos,
+                                     lane);
             }
             if (warp != 0) continue;
             if (gbest != kNone) {
@@ -652,7 +725,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
             // place (R6)
             const uint32_t rpos = r0.x, rar = r0.y, rfr = r0.z, rap = r0.w, rfp = r1.x,
                            rk = r1.y;
-            if (NW == 1) rr = retire_load(win, rpos, lane);  // overlaps the update
+            if (NW == 1) rr = retire_load<(TIER < TIER_SKEL)>(win, rpos, lane);  // overlaps the update
             HT rsz = (HT)r1.z;
             if (sizeof(HT) == 8) rsz |= (HT)((uint64_t)r1.w << 32);
             const HT ch = KO::h(ck);
