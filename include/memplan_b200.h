@@ -196,6 +196,14 @@ int mp_torch_epoch_reset(void); /* start a new replay epoch (Arena.reset) */
  * frees the region. */
 int mp_torch_replay_begin(mp_arena *arena, int device, uint64_t *base_out);
 int mp_torch_replay_end(void);
+/* Replay-mode counters since the last mode switch: requests served from the
+ * plan, requests served by side allocations, epochs that left the profiled
+ * order.  Replay places a block only when its allocation happens at its
+ * planned tick of the profile clock (profiler.py: +1 after every non-zero
+ * allocation and every free of one) and stops placing for the rest of the
+ * epoch once a free happens off its planned tick, so a run that deviates
+ * from the profile can never alias live memory. */
+int mp_torch_stats(int64_t *n_planned, int64_t *n_side, int64_t *n_diverged);
 /* Benchmark helper: replay the epoch `reps` times through mp_torch_alloc /
  * mp_torch_free directly (replay mode), best mean host ns per alloc call. */
 int mp_torch_bench(const int32_t *kinds, const int64_t *values, int64_t n_events, int64_t reps,

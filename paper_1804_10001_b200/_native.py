@@ -104,6 +104,7 @@ SIGNATURES = [
     ("mp_torch_epoch_reset", ctypes.c_int, []),
     ("mp_torch_replay_begin", ctypes.c_int, [VP, ctypes.c_int, PU64]),
     ("mp_torch_replay_end", ctypes.c_int, []),
+    ("mp_torch_stats", ctypes.c_int, [P64, P64, P64]),
     ("mp_torch_bench", ctypes.c_int, [VP, VP, ctypes.c_int64, ctypes.c_int64,
                                       ctypes.POINTER(ctypes.c_double)]),
     ("mp_pool_create", ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(VP)]),

@@ -498,6 +498,18 @@ struct TorchState {
     std::vector<int64_t> slot_ref;
     uint64_t span = 0, gran = 1;
     int gshift = 0;
+    int64_t n_planned = 0, n_side = 0;  // replay-mode counters since the mode switch
+    int64_t n_diverged = 0;             // epochs that left the plan (see mp_torch_alloc)
+    // replay guard: the profile clock of profiler.py (y starts at 1, +1 after
+    // every non-zero allocation and every free of one); a planned block is
+    // only placed when its allocation happens at its planned tick, and a
+    // free off its planned tick ends planned placement for the epoch
+    int64_t clock = 1;
+    bool diverged = false;
+    // zero-size requests: no block id, no tick (profiler.py), but torch
+    // needs distinct pointers: hand out bytes of a small dummy region
+    char *zbase = nullptr;
+    int64_t zcap = 0, zcount = 0;
 };
 
 TorchState &ts() {
@@ -528,9 +540,18 @@ int mp_torch_replay_begin(mp_arena *arena, int device, uint64_t *base_out) {
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e != cudaSuccess) return mp::cuda_fail(e, "cudaMalloc(replay region)");
     arena->base = (uint64_t)(uintptr_t)p;
+    void *z = nullptr;
+    e = cudaMalloc(&z, 1 << 20);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return mp::cuda_fail(e, "cudaMalloc(zero-size region)");
+    }
     MP_TRY(mp_torch_set_mode(2, arena));
     std::lock_guard<std::mutex> g(s.mu);
     s.region = p;
+    s.zbase = static_cast<char *>(z);
+    s.zcap = 1 << 20;
+    s.zcount = 0;
     if (base_out) *base_out = arena->base;
     return MP_OK;
 }
@@ -542,6 +563,11 @@ int mp_torch_replay_end(void) {
     if (s.region) {
         cudaFree(s.region);
         s.region = nullptr;
+    }
+    if (s.zbase) {
+        cudaFree(s.zbase);
+        s.zbase = nullptr;
+        s.zcap = 0;
     }
     return MP_OK;
 }
@@ -560,6 +586,11 @@ int mp_torch_set_mode(int mode, mp_arena *arena) {
     s.ptr_ref.clear();
     s.slot_ref.clear();
     s.n_allocs = 0;
+    s.n_planned = 0;
+    s.n_side = 0;
+    s.n_diverged = 0;
+    s.clock = 1;
+    s.diverged = false;
     if (mode == 2) {
         // planned addresses are base + (multiples of the alignment): index the
         // live blocks directly when the table stays small
@@ -599,6 +630,9 @@ int mp_torch_epoch_reset(void) {
     s.n_allocs = 0;
     s.ptr_ref.clear();
     std::fill(s.slot_ref.begin(), s.slot_ref.end(), 0);
+    if (s.diverged) s.n_diverged++;
+    s.clock = 1;
+    s.diverged = false;
     if (s.mode == 2 && s.arena) return s.arena->reset();
     return MP_OK;
 }
@@ -609,14 +643,19 @@ void *mp_torch_alloc(size_t size, int device, mp_stream_t stream) {
     std::lock_guard<std::mutex> g(s.mu);
     if (s.mode == 2 && s.arena) {
         mp_arena *a = s.arena;
+        if (size == 0 && s.zbase) return s.zbase + (s.zcount++ % s.zcap);
         const int64_t bid = a->lam;
         const int64_t sz = (int64_t)size;
-        if (device == s.device && a->depth == 0 && !a->closed && bid <= a->nblocks() &&
-            sz <= a->expected[bid] && sz > 0) {
+        const bool on_plan = !s.diverged && device == s.device && a->depth == 0 && !a->closed &&
+                             bid <= a->nblocks() && a->dalloc[bid] == s.clock;
+        if (!on_plan && sz > 0) s.diverged = true;
+        s.clock += sz > 0 ? 1 : 0;
+        if (on_plan && sz <= a->expected[bid] && sz > 0) {
             // hot path: base + offset[lambda] and one table store for the free
             uint64_t addr = 0;
             if (a->alloc(sz, &addr) == MP_OK) {
                 s.n_allocs++;
+                s.n_planned++;
                 const int64_t ref = (int64_t)a->seq.size();
                 const uint64_t rel = addr - a->base;
                 if (!s.slot_ref.empty() && rel < s.span && (rel & (s.gran - 1)) == 0)
@@ -626,7 +665,8 @@ void *mp_torch_alloc(size_t size, int device, mp_stream_t stream) {
                 return (void *)addr;
             }
         }
-        // outside the plan: live tensors cannot move, so serve from a side
+        // outside the plan (growth, extra request, or the run left the
+        // profiled order): live tensors cannot move, so serve from a side
         // allocation and remember the observed size for the next re-plan
         if (a->depth == 0 && bid <= a->nblocks() && sz > a->observed[bid]) a->observed[bid] = sz;
         int cur = -1;
@@ -634,8 +674,10 @@ void *mp_torch_alloc(size_t size, int device, mp_stream_t stream) {
         if (cur != device) cudaSetDevice(device);
         void *p = nullptr;
         if (cudaMalloc(&p, size ? size : 1) != cudaSuccess) return nullptr;
-        s.side[(uintptr_t)p] = ++s.n_allocs;
-        if (a->depth == 0) a->lam++;
+        s.side[(uintptr_t)p] = sz;
+        s.n_allocs++;
+        s.n_side++;
+        if (a->depth == 0 && sz > 0) a->lam++;
         return p;
     }
     int cur = -1;
@@ -660,22 +702,33 @@ void mp_torch_free(void *ptr, size_t size, int device, mp_stream_t stream) {
     if (s.mode == 2 && s.arena) {
         mp_arena *a = s.arena;
         const uint64_t rel = (uint64_t)(uintptr_t)ptr - a->base;
+        if (s.zbase && (char *)ptr >= s.zbase && (char *)ptr < s.zbase + s.zcap) return;
+        int64_t ref = 0;
         if (!s.slot_ref.empty() && rel < s.span && (rel & (s.gran - 1)) == 0) {
-            int64_t &ref = s.slot_ref[rel >> s.gshift];
-            if (ref > 0) {  // hot path: a planned block
-                a->free_ref(ref);
-                ref = 0;
-                return;
+            int64_t &r = s.slot_ref[rel >> s.gshift];
+            ref = r;
+            r = 0;
+        }
+        if (ref <= 0) {
+            auto jt = s.ptr_ref.find((uintptr_t)ptr);
+            if (jt != s.ptr_ref.end()) {
+                ref = jt->second;
+                s.ptr_ref.erase(jt);
             }
         }
-        auto jt = s.ptr_ref.find((uintptr_t)ptr);
-        if (jt != s.ptr_ref.end()) {
-            a->free_ref(jt->second);
-            s.ptr_ref.erase(jt);
-            return;  // planned memory is owned by the arena region
+        if (ref > 0) {  // hot path: a planned block (memory stays in the region)
+            const auto &e = a->seq[ref - 1];
+            if (!s.diverged && e.first == K_MANAGED && a->dfree[e.second] != s.clock)
+                s.diverged = true;
+            s.clock++;
+            a->free_ref(ref);
+            return;
         }
         auto it = s.side.find((uintptr_t)ptr);
-        if (it != s.side.end()) s.side.erase(it);
+        if (it != s.side.end()) {
+            if (it->second > 0) s.clock++;
+            s.side.erase(it);
+        }
         cudaFree(ptr);  // a side allocation, or a passthrough one made before replay
         return;
     }
@@ -688,6 +741,15 @@ void mp_torch_free(void *ptr, size_t size, int device, mp_stream_t stream) {
         }
     }
     cudaFree(ptr);
+}
+
+int mp_torch_stats(int64_t *n_planned, int64_t *n_side, int64_t *n_diverged) {
+    TorchState &s = ts();
+    std::lock_guard<std::mutex> g(s.mu);
+    if (n_planned) *n_planned = s.n_planned;
+    if (n_side) *n_side = s.n_side;
+    if (n_diverged) *n_diverged = s.n_diverged + (s.diverged ? 1 : 0);
+    return MP_OK;
 }
 
 int mp_torch_bench(const int32_t *kinds, const int64_t *values, int64_t n_events, int64_t reps,
