@@ -76,8 +76,9 @@ typedef struct {
     int64_t launches;     /* kernels launched by this call                  */
     int64_t diag[4];      /* with MP_STATS: choose scans, skeleton passes,
                              table segments read, edge rows read           */
-    int64_t cycles[4];    /* with env MEMPLAN_TIMING: SM cycles spent in the
-                             choose / query / update / retire phases        */
+    int64_t cycles[6];    /* with env MEMPLAN_TIMING: SM cycles spent in the
+                             choose / query / update / retire phases, and in
+                             lift / place steps                             */
 } mp_plan_info;
 
 /* ---- planning: replaces solve_bestfit(instance) -> Plan (bestfit.py:276) */

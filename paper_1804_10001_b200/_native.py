@@ -50,7 +50,7 @@ class PlanInfo(ctypes.Structure):
                 ("plan_ms", ctypes.c_float), ("kernel_ms", ctypes.c_float),
                 ("engine", ctypes.c_int32), ("cluster", ctypes.c_int32),
                 ("sum_wlive", ctypes.c_int64), ("launches", ctypes.c_int64),
-                ("diag", ctypes.c_int64 * 4), ("cycles", ctypes.c_int64 * 4)]
+                ("diag", ctypes.c_int64 * 4), ("cycles", ctypes.c_int64 * 6)]
 
 
 class VerifyReportC(ctypes.Structure):

@@ -69,7 +69,8 @@ def plan_info() -> dict:
     out = {name: getattr(info, name) for name, _ in N.PlanInfo._fields_
            if name not in ("diag", "cycles")}
     out["cycles"] = {"choose": info.cycles[0], "query": info.cycles[1],
-                     "update": info.cycles[2], "retire": info.cycles[3]}
+                     "update": info.cycles[2], "retire": info.cycles[3],
+                     "lift_steps": info.cycles[4], "place_steps": info.cycles[5]}
     out["diag"] = {"scans": info.diag[0], "passes": info.diag[1], "segments": info.diag[2],
                    "edge_rows": info.diag[3]}
     return out

@@ -314,7 +314,9 @@ __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint
     bool need = false;
     uint32_t code = 0, pe = kNone;
     if (valid) {
-        // all three skeleton records at once: one memory round
+        // all three skeleton records at once: one memory round (loading
+        // S1/S2 only for straddling chunks costs more in rounds than it
+        // saves in bytes, measured at 8 and 28 traces per SM)
         const uint4 q = ldk<SG>(w.s0 + j, w.keep);  // {K0, A, P, K15}
         const uint4 r = ldk<SG>(w.s1 + j, w.stream);  // {K7, K23, P7, P15}
         const uint32_t p23 = ldk<SG>(w.s2 + j, w.stream);
@@ -589,8 +591,9 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     bool hasP = false, hasN = false;
     uint32_t clop = 0, chip = 0, chi = 0, craw = 0, rawhi = 0;
 
-    long long tph[4] = {0, 0, 0, 0};  // timing: choose, query, update, retire
-    long long tc = a.timing ? clock64() : 0;
+    // timing: choose, query, update, retire phases; lift / place step totals
+    long long tph[6] = {0, 0, 0, 0, 0, 0};
+    long long tc = a.timing ? clock64() : 0, tstep = tc;
     for (;;) {
         // ======== leader: choose (R3) ========
         if (warp == 0) {
@@ -805,7 +808,12 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         if (a.timing) { const long long t2 = clock64(); tph[2] += t2 - tc; tc = t2; }
         if (NW == 1 && gbest != kNone) retire_finish<STATS>(win, rr, r0.x, lane);
         __syncwarp();
-        if (a.timing) { const long long t2 = clock64(); tph[3] += t2 - tc; tc = t2; }
+        if (a.timing) {
+            const long long t2 = clock64();
+            tph[3] += t2 - tc;
+            tph[gbest == kNone ? 4 : 5] += t2 - tstep;
+            tc = tstep = t2;
+        }
     }
     if (STATS && NW > 1) {
         if (lane == 0) {
@@ -830,7 +838,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         st[ST_PASS] = (int64_t)qs.pass;
         st[ST_SEG] = (int64_t)qs.seg;
         st[ST_EDGE] = (int64_t)qs.edge;
-        for (int k = 0; k < 4; k++) st[ST_T0 + k] = tph[k];
+        for (int k = 0; k < 6; k++) st[ST_T0 + k] = tph[k];
     }
 }
 
@@ -1145,7 +1153,7 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
         g_info.lifts += hst[t * ST_N + ST_LIFTS];
         g_info.sum_wlive += hst[t * ST_N + ST_WLIVE];
         for (int k = 0; k < 4; k++) g_info.diag[k] += hst[t * ST_N + ST_SCAN + k];
-        for (int k = 0; k < 4; k++) g_info.cycles[k] += hst[t * ST_N + ST_T0 + k];
+        for (int k = 0; k < 6; k++) g_info.cycles[k] += hst[t * ST_N + ST_T0 + k];
         g_info.max_lines = std::max(g_info.max_lines, hst[t * ST_N + ST_MAXLINES]);
         int64_t stv = hst[t * ST_N + ST_STATUS];
         if (stv == PS_LOOP_BOUND) {

@@ -127,8 +127,8 @@ __device__ __forceinline__ uint32_t skel_store(uint32_t key, uint32_t pr, int la
 enum {
     ST_STEPS = 0, ST_LIFTS = 1, ST_MAXLINES = 2, ST_STATUS = 3, ST_WLIVE = 4,
     ST_SCAN = 5, ST_PASS = 6, ST_SEG = 7, ST_EDGE = 8,
-    ST_T0 = 9,  // 4 slots: clock64() sums per phase with MEMPLAN_TIMING
-    ST_N = 13
+    ST_T0 = 9,  // 6 slots: clock64() sums per phase / step kind with MEMPLAN_TIMING
+    ST_N = 15
 };
 
 // Planner status values written to stats[ST_STATUS].

@@ -42,5 +42,8 @@ for n in sizes:
                   f"maxl={i['max_lines']} exact={ok} lifts={d['lifts']} "
                   f"wlive/step={d['sum_wlive'] / d['steps']:.0f} diag/step="
                   + " ".join(f"{k}={v / d['steps']:.2f}" for k, v in d['diag'].items())
-                  + " cyc/step " + " ".join(f"{k}={v / d['steps']:.0f}" for k, v in cyc.items()),
+                  + " cyc/step " + " ".join(f"{k}={v / d['steps']:.0f}" for k, v in cyc.items()
+                                            if not k.endswith("_steps"))
+                  + f" cyc/lift={cyc['lift_steps'] / max(1, d['lifts']):.0f}"
+                  + f" cyc/place={cyc['place_steps'] / max(1, d['steps'] - d['lifts']):.0f}",
                   flush=True)
