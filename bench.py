@@ -218,6 +218,26 @@ def config_suite(cpu_procs: int) -> dict:
                     "cpu_port_1core_ms": 1e3 * cpu_wall,
                     "speedup_vs_1core": cpu_wall / wall,
                     "bit_exact_vs_oracle": bool(np.array_equal(off, ref_off) and pk == ref_pk)}
+    # K3 validator (verify_plan, verifier.py:44-81): the reference builds the
+    # colliding-pair set as Python tuples (|E| ~ n^2/4) and cannot run at
+    # 10^5; the GPU checks every colliding pair.  CPU side: the C oracle.
+    from paper_1804_10001_b200.verifier import verify_arrays
+    from paper_1804_10001_b200.workloads import uniform_arrays
+    for n in (10000, 100000):
+        a, f, s = uniform_arrays(n, 0)
+        s = ((s + ALIGN - 1) // ALIGN) * ALIGN
+        off, pk = solve_bestfit_arrays(a, f, s)
+        verify_arrays(a, f, s, off)
+        wall, r = _best_wall(lambda: verify_arrays(a, f, s, off), 3)
+        rec = {"blocks": n, "gpu_host_to_host_ms": 1e3 * wall,
+               "valid": r["n_violations"] == 0 and r["offsets_ok"] and r["peak_recomputed"] == pk}
+        if n <= 10000:
+            cw, cr = _best_wall(lambda: oracle.verify(a, f, s, off), 1)
+            rec["cpu_c_oracle_1core_ms"] = 1e3 * cw
+            rec["agrees_with_oracle"] = (cr["n_violations"] == r["n_violations"] and
+                                         cr["peak_recomputed"] == r["peak_recomputed"] and
+                                         cr["used"] == r["used"])
+        out[f"verify_uniform_{n}"] = rec
     # configs[3]: 4096 variable-length LSTM seq2seq profiles planned batched
     from paper_1804_10001_b200.workloads import lstm_profiles
     profs = lstm_profiles(4096, layers=6, batch=64)

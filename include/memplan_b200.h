@@ -52,7 +52,8 @@ typedef enum {
     MP_ERR_UNBALANCED_RESUME = 11,/* UnbalancedResume, core.py:47-48           */
     MP_ERR_INVALID_PLAN = 12,     /* InvalidPlan, arena.py:35-36               */
     MP_ERR_OUT_OF_MEMORY = 13,    /* OutOfMemory (pool), arena.py:55-56        */
-    MP_ERR_NEGATIVE_SIZE = 14     /* ValueError on negative request size       */
+    MP_ERR_NEGATIVE_SIZE = 14,    /* ValueError on negative request size       */
+    MP_ERR_TRACE = 15             /* trace ingest error, see mp_ingest_info    */
 } mp_status;
 
 enum {
@@ -125,6 +126,29 @@ int mp_verify(const int64_t *alloc, const int64_t *free_, const int64_t *size,
 int mp_clique_lower_bound(const int64_t *alloc, const int64_t *free_,
                           const int64_t *size, int64_t n, int64_t *lb_out,
                           int flags, int device, mp_stream_t stream);
+
+/* ---- host ingest: replaces parse_trace + record + the block columns of
+ * profile_to_instance (profiler.py:97-231, core.py:184-224) ----------------
+ * One pass over ASCII trace text ("A size [label]", "F k", "I", "R", "#"
+ * comments).  Outputs the planned blocks in id order: aligned size, alloc
+ * and free clock ticks (cap = capacity of the three arrays).  On
+ * MP_ERR_TRACE, err_kind says which reference exception applies (the facade
+ * formats the reference's message): 1 "A needs a size", 2 bad size (token
+ * at err_tok_off/len), 3 NegativeSize (err_value), 4 "F needs exactly one
+ * block ref", 5 bad block ref (token), 6 ref < 1 (err_value), 7/8 "I"/"R"
+ * take no arguments, 9 unknown directive (token), 10 UnknownBlockRef
+ * (err_value, err_seen), 11 DoubleFree (err_value), 12 UnbalancedResume,
+ * 13 outside the ASCII / int64 restatement: use the Python path.  Syntax
+ * errors carry err_line and take precedence over recording errors, as in
+ * the two-stage reference. */
+typedef struct {
+    int64_t n_blocks, unmanaged_count, horizon, n_events;
+    int64_t err_line, err_tok_off, err_tok_len, err_value, err_seen;
+    int32_t err_kind, pad;
+} mp_ingest_info;
+
+int mp_ingest_trace(const char *text, int64_t len, int64_t alignment, int64_t *size_out,
+                    int64_t *alloc_out, int64_t *free_out, int64_t cap, mp_ingest_info *info);
 
 /* ---- replay arena: replaces Arena (arena.py:146-322) ---------------------
  * Opens over a plan; copies the tables.  `alignment` is the instance

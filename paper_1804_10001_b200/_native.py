@@ -32,6 +32,7 @@ MP_ERR_UNBALANCED_RESUME = 11
 MP_ERR_INVALID_PLAN = 12
 MP_ERR_OUT_OF_MEMORY = 13
 MP_ERR_NEGATIVE_SIZE = 14
+MP_ERR_TRACE = 15
 
 MP_DEVICE_PTRS = 1
 MP_ASYNC = 2
@@ -65,6 +66,13 @@ class ArenaState(ctypes.Structure):
         "n_live", "depth", "plan_version", "pool_last_ref")]
 
 
+class IngestInfo(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int64) for name in (
+        "n_blocks", "unmanaged_count", "horizon", "n_events", "err_line", "err_tok_off",
+        "err_tok_len", "err_value", "err_seen")] + [("err_kind", ctypes.c_int32),
+                                                     ("pad", ctypes.c_int32)]
+
+
 VIOLATION_DTYPE = np.dtype([("i", np.int64), ("j", np.int64),
                             ("overlap_bytes", np.int64), ("overlap_ticks", np.int64)])
 
@@ -79,6 +87,8 @@ SIGNATURES = [
                                  VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int, VP]),
     ("mp_clique_lower_bound", ctypes.c_int, [VP, VP, VP, ctypes.c_int64, P64, ctypes.c_int,
                                              ctypes.c_int, VP]),
+    ("mp_ingest_trace", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, VP, VP,
+                                       VP, ctypes.c_int64, ctypes.POINTER(IngestInfo)]),
     ("mp_arena_open", ctypes.c_int, [VP, VP, VP, VP, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_uint64, ctypes.c_int64, ctypes.c_int,
                                      ctypes.c_int, ctypes.POINTER(VP)]),
