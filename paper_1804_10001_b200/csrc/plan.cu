@@ -451,8 +451,8 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
     if (edge && (ek & 31u) >= (clop & 31u) && ek <= thr) best = min(best, ep);
     // provisional warp winner: prefetch its record while the segments load
     const uint32_t wb1 = __reduce_min_sync(kFull, best);
-    if (best == wb1 && best != kNone) {
-        load_rec(rec4, raw2, best, rec_smem, w.stream, r0, r1, rw);
+    if (!rec_smem && best == wb1 && best != kNone) {
+        load_rec(rec4, raw2, best, false, w.stream, r0, r1, rw);
     }
     if (!np) {
         lbest = best;
@@ -465,14 +465,14 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
     const uint32_t b2 = drain_pending(w, pend, np, thr, wb1, lane);
     if (b2 < best) best = b2;
     const uint32_t wb = __reduce_min_sync(kFull, best);
-    if (wb != wb1 && best == wb) {  // a pending segment improved it
-        load_rec(rec4, raw2, best, rec_smem, w.stream, r0, r1, rw);
+    if (!rec_smem && wb != wb1 && best == wb) {  // a pending segment improved it
+        load_rec(rec4, raw2, best, false, w.stream, r0, r1, rw);
     }
     lbest = best;
     return wb;
 }
 
-template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER>
+template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER, bool TIMING>
 __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     using KO = KeyT<HT>;
     using K = typename KO::K;
@@ -558,7 +558,11 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         win.sp = a.sp + 32 * cb;
     }
     const uint4 *rec4;
+    const uint2 *raw2 = a.raw2 + base;
     if (a.rec_smem) {
+        uint2 *rdst = reinterpret_cast<uint2 *>(smem + off + (size_t)n * 32);
+        for (int i = threadIdx.x; i < n; i += 32 * NW) rdst[i] = raw2[i];
+        raw2 = rdst;
         uint4 *dst = reinterpret_cast<uint4 *>(smem + off);
         const uint4 *src = reinterpret_cast<const uint4 *>(a.rec + base);
         for (int i = threadIdx.x; i < 2 * n; i += 32 * NW) dst[i] = src[i];
@@ -593,7 +597,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
 
     // timing: choose, query, update, retire phases; lift / place step totals
     long long tph[6] = {0, 0, 0, 0, 0, 0};
-    long long tc = a.timing ? clock64() : 0, tstep = tc;
+    long long tc = TIMING ? clock64() : 0, tstep = tc;
     for (;;) {
         // ======== leader: choose (R3) ========
         if (warp == 0) {
@@ -645,7 +649,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         if (NW > 1) __syncthreads();  // [A] choice published
         if (NW > 1 ? ss.done : (placed >= n || status != PS_OK)) break;
 
-        if (a.timing) { const long long t2 = clock64(); tph[0] += t2 - tc; tc = t2; }
+        if (TIMING) { const long long t2 = clock64(); tph[0] += t2 - tc; tc = t2; }
         // ======== all warps: query (R4) ========
         uint32_t qlop, qhip, qchi, qraw;
         if (NW > 1) { qlop = ss.clop; qhip = ss.chip; qchi = ss.chi; qraw = ss.rawhi; }
@@ -655,7 +659,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         uint2 rw = make_uint2(0, 0);
         if (qlop < qhip) {
             const int c0 = (int)(qlop >> 5), c1 = (int)((qhip - 1) >> 5);
-            wb = query_window<STATS, NW, TIER>(win, rec4, a.raw2 + base, pend, c0, c1, qchi, qlop,
+            wb = query_window<STATS, NW, TIER>(win, rec4, raw2, pend, c0, c1, qchi, qlop,
                                                qhip, qraw, prune, warp, lane, lbest, r0, r1, rw,
                                                qs, a.rec_smem != 0);
         }
@@ -672,22 +676,32 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
             gbest = __reduce_min_sync(kFull, mine);
             int ww = -1;
             if (gbest != kNone) ww = __ffs(__ballot_sync(kFull, mine == gbest)) - 1;
+            if (gbest != kNone) {
+                if (a.rec_smem) {
+                    r0 = rec4[2 * gbest];
+                    r1 = rec4[2 * gbest + 1];
+                    rw = raw2[gbest];
+                } else {
+                    r0 = ss.wrec[ww][0];
+                    r1 = ss.wrec[ww][1];
+                    rw = ss.wraw[ww];
+                }
+            }
             if (ww == warp) {
                 // the winning warp retires the entry while the leader
                 // rewrites the skyline (both finish before barrier [A])
-                const uint32_t pos = ss.wrec[warp][0].x;
+                const uint32_t pos = r0.x;
                 retire_finish<STATS>(win, retire_load<(TIER < TIER_SKEL)>(win, pos, lane), pos,
                                      lane);
             }
             if (warp != 0) continue;
-            if (gbest != kNone) {
-                r0 = ss.wrec[ww][0];
-                r1 = ss.wrec[ww][1];
-                rw = ss.wraw[ww];
-            }
         } else {
             gbest = wb;
-            if (gbest != kNone) {
+            if (gbest != kNone && a.rec_smem) {
+                r0 = rec4[2 * gbest];  // shared memory broadcast reads
+                r1 = rec4[2 * gbest + 1];
+                rw = raw2[gbest];
+            } else if (gbest != kNone) {
                 const int src = __ffs(__ballot_sync(kFull, lbest == gbest)) - 1;
                 r0.x = __shfl_sync(kFull, r0.x, src);
                 r0.y = __shfl_sync(kFull, r0.y, src);
@@ -702,7 +716,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
             }
         }
 
-        if (a.timing) { const long long t2 = clock64(); tph[1] += t2 - tc; tc = t2; }
+        if (TIMING) { const long long t2 = clock64(); tph[1] += t2 - tc; tc = t2; }
         // ======== leader: replacement of lines [c, c+e] by m new lines ========
         K nk0 = 0, nk1 = 0, nk2 = 0;
         uint32_t np0 = 0, np1 = 0, np2 = 0, nr0 = 0, nr1 = 0, nr2 = 0;
@@ -805,10 +819,10 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         nl += d;
         maxl = max(maxl, nl);
         c = cnext;
-        if (a.timing) { const long long t2 = clock64(); tph[2] += t2 - tc; tc = t2; }
+        if (TIMING) { const long long t2 = clock64(); tph[2] += t2 - tc; tc = t2; }
         if (NW == 1 && gbest != kNone) retire_finish<STATS>(win, rr, r0.x, lane);
         __syncwarp();
-        if (a.timing) {
+        if (TIMING) {
             const long long t2 = clock64();
             tph[3] += t2 - tc;
             tph[gbest == kNone ? 4 : 5] += t2 - tstep;
@@ -846,11 +860,12 @@ thread_local int64_t g_launches = 0;
 thread_local int g_nwarps = 1;  // warps per trace chosen by plan_device
 thread_local int g_carveout = -1;  // shared-memory carveout percent (-1: driver default)
 
-template <typename HT, bool Ls, bool ST, int NW, int TIER>
-int launch_k(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
-    auto fn = k_plan<HT, Ls, ST, NW, TIER>;
-    if (smem > 48 * 1024)
-        MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <typename HT, bool Ls, bool ST, int NW, int TIER, bool TM>
+int launch_kt(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
+    auto fn = k_plan<HT, Ls, ST, NW, TIER, TM>;
+    // always opt in: dynamic + static shared memory may pass 48 KB even when
+    // the dynamic part alone does not
+    MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // keep only the shared memory the resident CTAs need: the rest is L1,
     // which caches the L2-resident window table between steps
     MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout));
@@ -858,6 +873,16 @@ int launch_k(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
     MP_CUDA(cudaGetLastError());
     g_launches++;
     return MP_OK;
+}
+
+// Phase timing (MEMPLAN_TIMING) is compiled only into the single-warp,
+// 32-bit-height, shared-memory-lines kernels that the latency study uses.
+template <typename HT, bool Ls, bool ST, int NW, int TIER>
+int launch_k(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
+    if constexpr (sizeof(HT) == 4 && Ls && !ST && NW == 1) {
+        if (a.timing) return launch_kt<HT, Ls, ST, NW, TIER, true>(a, grid, smem, s);
+    }
+    return launch_kt<HT, Ls, ST, NW, TIER, false>(a, grid, smem, s);
 }
 
 template <typename HT, bool Ls, bool ST, int TIER>
@@ -926,7 +951,7 @@ Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwar
     const size_t grp_b = (size_t)((nch + 31) / 32) * 16;
     const size_t skel_b = (size_t)nch * 32 + a16((size_t)nch * 4);
     const size_t tab_b = (size_t)nch * 32 * 8;
-    const size_t rec_b = (size_t)nmax * 32;
+    const size_t rec_b = (size_t)nmax * 40;  // records + raw alloc/free
     size_t used = pend_b;
     if (!force_global) {
         if (!lines_global && used + lines_b <= lim) { l.lines_smem = true; used += lines_b; }
