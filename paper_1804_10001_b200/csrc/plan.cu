@@ -65,7 +65,7 @@ struct PlanArgs {
     const int64_t *trace_ptr;
     uint32_t *sf, *sp;        // chunk-sorted window table (global), 32 per chunk
     uint4 *s0, *s1;           // chunk skeleton (global), see plan_types.cuh
-    uint32_t *s2;
+    uint2 *s2;
     uint4 *gs;                // group skeleton (global)
     uint32_t *cnt;            // live entries per chunk (STATS)
     const Rec *rec;           // N
@@ -143,7 +143,7 @@ template <typename K> struct __align__(16) LineRec {
 // Window structures of one trace (pointers already offset to its chunks).
 struct Win {
     uint4 *s0, *s1;      // chunk skeleton (shared or global)
-    uint32_t *s2;
+    uint2 *s2;
     uint4 *gs;           // group skeleton (shared or global)
     int nch;             // chunks of this trace
     uint32_t *sf, *sp;   // chunk-sorted table (shared or global)
@@ -308,18 +308,45 @@ struct QStats {
 // fold into `best`; a straddling chunk whose boundary segment may still win
 // is appended to the warp's pending list (code = j<<2 | segment, and the
 // segment's prefix minimum as the bound it must beat).
+// One chunk's skeleton records (loaded together: one memory round).
+struct ChunkSk {
+    uint4 q;   // {K0, A, P, K15}
+    uint4 r;   // {K7, K23, P7, P15}
+    uint2 q2;  // {P23, RA}
+    bool valid;
+};
+
+template <bool SG>
+__device__ __forceinline__ ChunkSk load_chunk(const Win &w, int j, bool valid) {
+    ChunkSk c;
+    c.valid = valid;
+    c.q = make_uint4(kNone, kNone, kNone, kNone);
+    c.r = make_uint4(0, 0, 0, 0);
+    c.q2 = make_uint2(0, 0);
+    if (valid) {
+        // loading S1/S2 only for straddling chunks costs more in rounds than
+        // it saves in bytes (measured at 8 and 28 traces per SM)
+        c.q = ldk<SG>(w.s0 + j, w.keep);
+        c.r = ldk<SG>(w.s1 + j, w.stream);
+        c.q2 = ldk<SG>(w.s2 + j, w.stream);
+    }
+    return c;
+}
+
 template <bool SG>
 __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint32_t thr,
-                                           uint32_t &best, uint32_t *pend, int &np, int lane) {
+                                           uint32_t rawhi, uint32_t lstar, uint32_t &best,
+                                           uint32_t *pend, int &np, int lane);
+
+__device__ __forceinline__ void eval_loaded(const ChunkSk &c, int j, uint32_t thr,
+                                            uint32_t rawhi, uint32_t lstar, uint32_t &best,
+                                            uint32_t *pend, int &np, int lane) {
     bool need = false;
     uint32_t code = 0, pe = kNone;
-    if (valid) {
-        // all three skeleton records at once: one memory round (loading
-        // S1/S2 only for straddling chunks costs more in rounds than it
-        // saves in bytes, measured at 8 and 28 traces per SM)
-        const uint4 q = ldk<SG>(w.s0 + j, w.keep);  // {K0, A, P, K15}
-        const uint4 r = ldk<SG>(w.s1 + j, w.stream);  // {K7, K23, P7, P15}
-        const uint32_t p23 = ldk<SG>(w.s2 + j, w.stream);
+    if (c.valid) {
+        const uint4 q = c.q, r = c.r;
+        const uint2 q2 = c.q2;
+        const uint32_t p23 = q2.x;
         if (q.x <= thr) {
             if (q.y <= thr) {
                 best = min(best, q.z);  // the chunk's best live entry fits
@@ -335,7 +362,10 @@ __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint
                     else { s = 0; pb = kNone; pe = r.z; }
                 }
                 best = min(best, pb);  // slots before segment s all fit
-                if (pe < best) {       // segment s may still hold a better fit
+                // segment s may still hold a better fit: its prefix minimum
+                // must beat the best, and (lifetime bound) a block of this
+                // chunk that fits lives at most rawhi - RA
+                if (pe < best && rawhi - q2.y >= lstar) {
                     need = true;
                     code = ((uint32_t)j << 2) | s;
                 }
@@ -351,6 +381,14 @@ __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint
         }
         np += __popc(m);
     }
+}
+
+template <bool SG>
+__device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint32_t thr,
+                                           uint32_t rawhi, uint32_t lstar, uint32_t &best,
+                                           uint32_t *pend, int &np, int lane) {
+    const ChunkSk c = load_chunk<SG>(w, j, valid);
+    eval_loaded(c, j, thr, rawhi, lstar, best, pend, np, lane);
 }
 
 // Best contained block among the window chunks this warp handles (rule R4).
@@ -402,10 +440,17 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
         if (warp == 0) {
             const int j = cs + lane;
             if (STATS) qs.pass++;
-            eval_chunk<(TIER < TIER_SKEL)>(w, j, j <= c1 && j < 32 * gf, thr, best, pend, np,
-                                            lane);
+            eval_chunk<(TIER < TIER_SKEL)>(w, j, j <= c1 && j < 32 * gf, thr, rawhi, 0u, best,
+                                            pend, np, lane);
+            if (np > kPendCap - 32 * 4) {
+                if (STATS) qs.seg += np;
+                best = min(best, drain_pending(w, pend, np, thr, kNone, lane));
+                np = 0;
+            }
         }
     }
+    // lifetime bound of the best candidate so far (0 = none yet)
+    uint32_t lstar = 0, e_used = kNone;
     // whole groups [gf, c1 >> 5] (none when the window is the edge chunk alone)
     const int gl = cs <= c1 ? c1 >> 5 : gf - 1;
     for (int gb = gf + 32 * warp; gb <= gl; gb += 32 * NW) {
@@ -421,30 +466,52 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
             }
         }
         unsigned m = __ballot_sync(kFull, scan);
-        if (prune && __popc(m) >= 3) {
-            // Lifetime bound: a block of group g that fits [lo, hi) lives at
-            // most rawhi - GR(g).  Priority order is lifetime-major, so a
-            // group whose bound is below the lifetime of the best candidate
-            // so far cannot hold a better one (equal bounds are kept: size
-            // and id break lifetime ties).
+        // Lifetime bound: a block of group g that fits [lo, hi) lives at most
+        // rawhi - GR(g).  Priority order is lifetime-major, so a group whose
+        // bound is below the lifetime of the best candidate so far cannot
+        // hold a better one (equal bounds are kept: size and id break
+        // lifetime ties).  GR grows left to right, so once a group fails
+        // every group to its right fails too; flagged groups are scanned
+        // left to right and the bound is re-applied as the best improves.
+        auto tighten = [&]() {
             const uint32_t e = __reduce_min_sync(kFull, best);
-            if (e != kNone) {
-                const uint2 er = ldk<true>(raw2 + e, w.stream);
-                const uint32_t lstar = er.y - er.x;
-                m = __ballot_sync(kFull, scan && rawhi - graw >= lstar);
+            if (e < e_used) {
+                e_used = e;
+                const uint2 er = rec_smem ? raw2[e] : ldg_hint(raw2 + e, w.stream);
+                lstar = er.y - er.x;
+                m &= __ballot_sync(kFull, scan && rawhi - graw >= lstar);
             }
-        }
+        };
+        if (lstar) m &= __ballot_sync(kFull, scan && rawhi - graw >= lstar);
+        if (prune && __popc(m) >= 3) tighten();
         while (m) {
-            const int g2 = gb + __ffs(m) - 1;
-            m &= m - 1;
-            const int j = 32 * g2 + lane;
-            if (STATS) qs.pass++;
-            eval_chunk<(TIER < TIER_SKEL)>(w, j, j <= c1, thr, best, pend, np, lane);
-            if (np > kPendCap - 32) {
+            // up to four flagged groups per memory round (left to right)
+            constexpr int kG = 4;
+            ChunkSk ck4[kG];
+            int jj[kG];
+#pragma unroll
+            for (int u = 0; u < kG; u++) {
+                jj[u] = -1;
+                if (m) {
+                    const int g2 = gb + __ffs(m) - 1;
+                    m &= m - 1;
+                    jj[u] = 32 * g2 + lane;
+                }
+                ck4[u] = load_chunk<(TIER < TIER_SKEL)>(w, jj[u], jj[u] >= 0 && jj[u] <= c1);
+            }
+#pragma unroll
+            for (int u = 0; u < kG; u++) {
+                if (__any_sync(kFull, jj[u] >= 0)) {
+                    if (STATS) qs.pass++;
+                    eval_loaded(ck4[u], jj[u], thr, rawhi, lstar, best, pend, np, lane);
+                }
+            }
+            if (np > kPendCap - 32 * kG) {
                 if (STATS) qs.seg += np;
                 best = min(best, drain_pending(w, pend, np, thr, kNone, lane));
                 np = 0;
             }
+            if (prune && __popc(m) >= 4) tighten();
         }
     }
     // the speculative edge row has long arrived: fold it in first
@@ -528,15 +595,15 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     }
     if (TIER >= TIER_SKEL) {
         uint4 *d = reinterpret_cast<uint4 *>(smem + off);
-        off += (size_t)nch * 32 + align16((size_t)nch * 4);
+        off += (size_t)nch * 32 + align16((size_t)nch * 8);
         for (int i = threadIdx.x; i < nch; i += 32 * NW) {
             d[i] = a.s0[cb + i];
             d[nch + i] = a.s1[cb + i];
-            reinterpret_cast<uint32_t *>(d + 2 * nch)[i] = a.s2[cb + i];
+            reinterpret_cast<uint2 *>(d + 2 * nch)[i] = a.s2[cb + i];
         }
         win.s0 = d;
         win.s1 = d + nch;
-        win.s2 = reinterpret_cast<uint32_t *>(d + 2 * nch);
+        win.s2 = reinterpret_cast<uint2 *>(d + 2 * nch);
     } else {
         win.s0 = a.s0 + cb;
         win.s1 = a.s1 + cb;
@@ -949,7 +1016,7 @@ Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwar
     const size_t pend_b = (size_t)nwarps * 2 * kPendCap * sizeof(uint32_t);
     const int64_t nch = (nmax + 31) / 32;
     const size_t grp_b = (size_t)((nch + 31) / 32) * 16;
-    const size_t skel_b = (size_t)nch * 32 + a16((size_t)nch * 4);
+    const size_t skel_b = (size_t)nch * 32 + a16((size_t)nch * 8);
     const size_t tab_b = (size_t)nch * 32 * 8;
     const size_t rec_b = (size_t)nmax * 40;  // records + raw alloc/free
     size_t used = pend_b;
@@ -999,7 +1066,8 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     const size_t tab_b = Carver::need<uint2>(N) + Carver::need<Rec>(N) +
                          Carver::need<uint32_t>(T) + Carver::need<int64_t>(T) +
                          Carver::need<uint64_t>(T) + Carver::need<int64_t>(T * ST_N) +
-                         2 * Carver::need<uint4>(nchunks) + 2 * Carver::need<uint32_t>(nchunks) +
+                         2 * Carver::need<uint4>(nchunks) + Carver::need<uint2>(nchunks) +
+                         Carver::need<uint32_t>(nchunks) +
                          Carver::need<uint4>(ngroups) + Carver::need<uint2>(N) +
                          Carver::need<uint32_t>(N) + 2 * Carver::need<int64_t>(T) +
                          2 * Carver::need<uint32_t>(32 * nchunks);
@@ -1012,7 +1080,7 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     po.sp = cv.take<uint32_t>(32 * nchunks);
     po.s0 = cv.take<uint4>(nchunks);
     po.s1 = cv.take<uint4>(nchunks);
-    po.s2 = cv.take<uint32_t>(nchunks);
+    po.s2 = cv.take<uint2>(nchunks);
     po.nchunks = nchunks;
     po.gs = cv.take<uint4>(ngroups);
     po.ngroups = ngroups;

@@ -38,7 +38,8 @@ constexpr uint32_t kDead = 0xFFFFFFFFu;
 // the common case):
 //   S0 = {K0, A, P, K15}      (uint4)
 //   S1 = {K7, K23, P7, P15}   (uint4)
-//   S2 = P23                  (u32)
+//   S2 = {P23, RA}            (uint2; RA = raw alloc time of the chunk's
+//                             first position relative to the trace origin)
 //   K0        key of the first live slot (no live entry fits unless K0 <= thr)
 //   A, P      key and priority of the chunk's best live entry: if A <= thr
 //             the chunk's answer is exactly P
@@ -97,7 +98,7 @@ __device__ __forceinline__ void group_store(const uint4 *s0, int64_t nch, uint4 
 // lane = sorted slot, `key` = SF, `pr` = SP with retired / padding slots at
 // kDead).  Returns the live count.
 __device__ __forceinline__ uint32_t skel_store(uint32_t key, uint32_t pr, int lane, uint4 *s0,
-                                               uint4 *s1, uint32_t *s2, int64_t j,
+                                               uint4 *s1, uint2 *s2, int64_t j,
                                                uint4 *s0_out = nullptr) {
     constexpr unsigned full = 0xFFFFFFFFu;
     constexpr uint32_t none = 0xFFFFFFFFu;
@@ -114,7 +115,7 @@ __device__ __forceinline__ uint32_t skel_store(uint32_t key, uint32_t pr, int la
     if (lane == 0) {
         s0[j] = make_uint4(k0, a, p, k15);
         s1[j] = make_uint4(k7, k23, p7, p15);
-        s2[j] = p23;
+        s2[j].x = p23;  // S2.y (the chunk's raw alloc origin) is static
     }
     if (s0_out) *s0_out = make_uint4(k0, a, p, k15);
     return (uint32_t)__popc(live);

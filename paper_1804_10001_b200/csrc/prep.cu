@@ -288,7 +288,8 @@ __global__ void k_pack(const uint32_t *__restrict__ tix, const int64_t *__restri
 __global__ void k_chunk_sort(const int64_t *__restrict__ trace_ptr, int64_t T,
                              const uint2 *__restrict__ ent, uint32_t *__restrict__ sf,
                              uint32_t *__restrict__ sp, uint4 *__restrict__ s0,
-                             uint4 *__restrict__ s1, uint32_t *__restrict__ s2,
+                             uint4 *__restrict__ s1, uint2 *__restrict__ s2,
+                             const uint32_t *__restrict__ rawpos,
                              uint32_t *__restrict__ cnt, int64_t nchunks) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -327,6 +328,7 @@ __global__ void k_chunk_sort(const int64_t *__restrict__ trace_ptr, int64_t T,
         sf[32 * cg + lane] = key;
         sp[32 * cg + lane] = pr;
         const uint32_t nlive = skel_store(key, pr, lane, s0, s1, s2, cg);
+        if (lane == 0 && j < ((n + 31) >> 5)) s2[cg].y = rawpos[b + 32 * j];
         if (lane == 0) cnt[cg] = nlive;
     }
 }
@@ -516,7 +518,7 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
         const int64_t chunks = out.nchunks;
         const int blocks = (int)std::min<int64_t>((chunks + 7) / 8, 148 * 64);
         k_chunk_sort<<<blocks, 256, 0, s>>>(in.trace_ptr, T, out.ent, out.sf, out.sp, out.s0,
-                                            out.s1, out.s2, out.cnt, chunks);
+                                            out.s1, out.s2, out.rawpos, out.cnt, chunks);
         g_prep_k++;
         const int gblocks = (int)std::min<int64_t>((out.ngroups + 7) / 8, 148 * 64);
         k_group_skel<<<gblocks, 256, 0, s>>>(in.trace_ptr, T, out.s0, out.rawpos, out.gs,

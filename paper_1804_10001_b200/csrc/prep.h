@@ -18,7 +18,7 @@ struct PrepOut {
     // chunk-sorted table, 32 slots per chunk, chunk_base() indexing
     uint32_t *sf, *sp;
     uint4 *s0, *s1;        // chunk skeleton {K0,A,P,K15}, {K7,K23,P7,P15} per chunk
-    uint32_t *s2;          // chunk skeleton P23 per chunk
+    uint2 *s2;             // chunk skeleton {P23, raw alloc origin} per chunk
     int64_t nchunks;       // total chunks of the batch (incl. per-trace gaps)
     uint4 *gs;             // group skeleton per group of 32 chunks
     int64_t ngroups;       // total groups of the batch (incl. per-trace gaps)
