@@ -682,6 +682,23 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
                         const HT hmin = KO::warp_min_h(KO::h(k));
                         c = __ffs(__ballot_sync(kFull, KO::h(k) == hmin && lane < nl)) - 1;
                         ck = KO::make(hmin, __shfl_sync(kFull, KO::lo(k), c));
+                    } else if (nl <= 128) {
+                        // heights first (one reduction), then the leftmost
+                        // line at that height (a second reduction over line
+                        // indices); independent loads, depth-2 min trees
+                        HT hr[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int i = lane + 32 * u;
+                            hr[u] = i < nl ? KO::h(L[i].key) : ~HT(0);
+                        }
+                        const HT hmin = KO::warp_min_h(min(min(hr[0], hr[1]), min(hr[2], hr[3])));
+                        uint32_t ir[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++)
+                            ir[u] = hr[u] == hmin ? (uint32_t)(lane + 32 * u) : 0xFFFFFFFFu;
+                        c = (int)__reduce_min_sync(kFull, min(min(ir[0], ir[1]), min(ir[2], ir[3])));
+                        ck = L[c].key;
                     } else {
                         K bk = KO::none();
                         int bi = 0;

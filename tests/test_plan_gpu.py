@@ -82,3 +82,56 @@ def test_wide_heights_64bit():
     ooff, opeak = oracle.solve_bestfit(a, f, s)
     assert peak == opeak and np.array_equal(off, ooff)
     assert not (plan_info()["engine"] & 16)
+
+
+def test_huge_time_span_disables_lifetime_pruning():
+    """Raw times spread over 2^40 ticks: the planner's lifetime bounds (31-bit
+    relative times) switch off and the result must still be bit-exact."""
+    from paper_1804_10001_b200.bestfit import solve_bestfit_arrays
+    rng = np.random.default_rng(9)
+    n = 4000
+    a = rng.integers(0, 1 << 40, n)
+    f = a + 1 + rng.integers(0, 1 << 38, n)
+    s = rng.integers(1, 1 << 20, n)
+    off, peak = solve_bestfit_arrays(a, f, s)
+    ooff, opeak = oracle.solve_bestfit(a, f, s)
+    assert peak == opeak and np.array_equal(off, ooff)
+
+
+@pytest.mark.parametrize("flags", [0, 4])
+def test_edge_shapes(flags):
+    """Degenerate shapes: one block, identical blocks, nested, all disjoint,
+    a single long-lived block over many short ones."""
+    from paper_1804_10001_b200.bestfit import solve_bestfit_arrays
+    cases = [
+        ([0], [1], [7]),
+        ([0] * 50, [10] * 50, [3] * 50),
+        (list(range(40)), [80 - i for i in range(40)], [i + 1 for i in range(40)]),
+        ([2 * i for i in range(300)], [2 * i + 1 for i in range(300)], [5] * 300),
+        ([0] + list(range(1, 600)), [1000] + list(range(2, 601)), [1 << 30] + [1] * 599),
+    ]
+    for a, f, s in cases:
+        a, f, s = (np.asarray(x, np.int64) for x in (a, f, s))
+        off, peak = solve_bestfit_arrays(a, f, s, flags=flags)
+        ooff, opeak = oracle.solve_bestfit(a, f, s)
+        assert peak == opeak and np.array_equal(off, ooff)
+
+
+def test_large_batch_mixed_sizes():
+    """A batch mixing tiny, medium and 3*10^4-block traces (several layout
+    tiers in one launch) against the oracle."""
+    from paper_1804_10001_b200.bestfit import solve_bestfit_batched_arrays
+    from paper_1804_10001_b200.workloads import uniform_arrays
+    sizes = [0, 1, 13, 129, 2000, 30000, 7, 5000]
+    cols = []
+    for i, n in enumerate(sizes):
+        a, f, s = uniform_arrays(n, 100 + i) if n else (np.zeros(0, np.int64),) * 3
+        cols.append((a, f, ((s + 511) // 512) * 512))
+    tp = np.zeros(len(cols) + 1, np.int64)
+    np.cumsum([len(c[0]) for c in cols], out=tp[1:])
+    A = np.concatenate([c[0] for c in cols]); F = np.concatenate([c[1] for c in cols])
+    S = np.concatenate([c[2] for c in cols])
+    off, peaks = solve_bestfit_batched_arrays(tp, A, F, S)
+    for t, (a, f, s) in enumerate(cols):
+        ooff, opeak = oracle.solve_bestfit(a, f, s)
+        assert peaks[t] == opeak and np.array_equal(off[tp[t]:tp[t + 1]], ooff), t

@@ -1,0 +1,27 @@
+# compute-sanitizer memcheck / racecheck / synccheck on the planner, validator
+# and prep kernels over small traces (single and batched).
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+cat > /tmp/san_case.py <<'PY'
+import os, sys
+sys.path.insert(0, os.environ["GRAFT_REPO_ROOT"])
+import numpy as np
+import paper_1804_10001_b200 as mp
+from paper_1804_10001_b200.bestfit import solve_bestfit_arrays, solve_bestfit_batched_arrays
+from paper_1804_10001_b200.verifier import verify_arrays
+from paper_1804_10001_b200.workloads import uniform_arrays
+a, f, s = uniform_arrays(3000, 1); s = ((s + 511) // 512) * 512
+off, pk = solve_bestfit_arrays(a, f, s)
+solve_bestfit_arrays(a, f, s, flags=4)
+r = verify_arrays(a, f, s, off)
+assert r["n_violations"] == 0
+inst = mp.profile_to_instance(mp.record(mp.parse_trace(mp.cnn_like_trace(mp.GenSpec(model="cnn", layers=500, seed=0)))), alignment=512)
+solve_bestfit_arrays(*inst.arrays())
+tp = np.array([0, 1000, 1500, 3000]); solve_bestfit_batched_arrays(tp, a, f, s)
+k = np.arange(1200, dtype=np.int64); solve_bestfit_arrays(2 * k, 2 * k + 1, k + 1)
+print("case ok", pk)
+PY
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 3 python /tmp/san_case.py > gpurun_out/san_$tool.log 2>&1
+  echo "$tool rc=$?"; tail -n 3 gpurun_out/san_$tool.log
+done
