@@ -14,6 +14,10 @@ for n in sizes:
     for fam in fams:
         if fam == "uniform":
             a, f, s = uniform_arrays(n, 0); s = ((s + 511) // 512) * 512
+        elif fam in ("alexnet", "googlenet", "resnet50", "inception_resnet_v2"):
+            a, f, s = mp.profile_to_instance(mp.record(mp.parse_trace(mp.net_trace(fam, n))),
+                                             alignment=512).arrays()
+            n = len(a)
         else:
             a, f, s = mp.profile_to_instance(mp.record(mp.parse_trace(mp.cnn_like_trace(
                 mp.GenSpec(model="cnn", layers=n // 2, seed=0)))), alignment=512).arrays()
