@@ -39,6 +39,7 @@
 // The loop bound assert (R8, bestfit.py:297) and IllegalLift (:185-186)
 // are reported through the per-trace status word.
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -1026,7 +1027,7 @@ size_t lines_bytes(int lcap, size_t hbytes) {
 }
 
 Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwarps,
-                     bool force_global, bool lines_global = false) {
+                     bool force_global, bool lines_global = false, int max_tier = TIER_ALL) {
     Layout l{};
     l.tier = TIER_GLOBAL;
     const size_t lines_b = lines_bytes(lcap, hbytes);
@@ -1039,13 +1040,13 @@ Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwar
     size_t used = pend_b;
     if (!force_global) {
         if (!lines_global && used + lines_b <= lim) { l.lines_smem = true; used += lines_b; }
-        if (used + grp_b <= lim) {
+        if (max_tier >= TIER_GROUP && used + grp_b <= lim) {
             l.tier = TIER_GROUP;
             used += grp_b;
-            if (used + skel_b <= lim) {
+            if (max_tier >= TIER_SKEL && used + skel_b <= lim) {
                 l.tier = TIER_SKEL;
                 used += skel_b;
-                if (used + tab_b <= lim) {
+                if (max_tier >= TIER_ALL && used + tab_b <= lim) {
                     l.tier = TIER_ALL;
                     used += tab_b;
                     if (used + rec_b <= lim) { l.rec_smem = true; used += rec_b; }
@@ -1131,8 +1132,8 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     for (int64_t t = 0; t < T; t++) h32 = h32 && tot[t] < (uint64_t(1) << 32);
     const size_t hb = h32 ? 4 : 8;
 
-    // dynamic shared memory limit (the static StepShared block takes ~1.5 KB)
-    const size_t lim = smem_limit(device) - 2048;
+    // dynamic shared memory limit (the static StepShared block takes ~2.8 KB)
+    const size_t lim = smem_limit(device) - 4096;
     const bool force_global = (flags & MP_FORCE_GLOBAL) != 0;
     const int64_t lneed = 2 * nmax + 2;  // worst case 2n+1 lines
     // Layout policy.  A single trace (or fewer traces than SMs) gets the
@@ -1159,16 +1160,14 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     }
     if (const char *env = getenv("MEMPLAN_TIER")) {  // tuning: cap the shared-memory tier
         const int v = atoi(env);
-        if (v >= TIER_GLOBAL && v < lay.tier) {
-            lay = choose_layout(nmax, lcap_s, hb, budget, g_nwarps, force_global);
-            if (v <= TIER_GROUP) {
-                lay.tier = v;
-                lay.rec_smem = false;
-                lay.smem = lines_bytes(lcap_s, hb) + (size_t)g_nwarps * 2 * kPendCap * 4 +
-                           (v == TIER_GROUP ? (size_t)((nmax + 1023) / 1024) * 16 : 0);
-            }
-        }
+        if (v >= TIER_GLOBAL && v < lay.tier)
+            lay = choose_layout(nmax, lcap_s, hb, budget, g_nwarps, force_global, false, v);
     }
+    if (getenv("MEMPLAN_DEBUG_LAYOUT"))
+        fprintf(stderr, "memplan layout: nmax=%lld T=%lld nw=%d tier=%d lines_smem=%d rec_smem=%d "
+                        "smem=%zu budget=%zu lim=%zu lcap=%d\n",
+                (long long)nmax, (long long)T, g_nwarps, lay.tier, (int)lay.lines_smem,
+                (int)lay.rec_smem, lay.smem, budget, lim, lcap_s);
     {
         const int64_t per_sm = std::max<int64_t>(1, (T + sms - 1) / sms);
         const double need = (double)per_sm * (double)(lay.smem + 1024 + sizeof(void *) * 256);

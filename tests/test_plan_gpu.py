@@ -135,3 +135,29 @@ def test_large_batch_mixed_sizes():
     for t, (a, f, s) in enumerate(cols):
         ooff, opeak = oracle.solve_bestfit(a, f, s)
         assert peaks[t] == opeak and np.array_equal(off[tp[t]:tp[t + 1]], ooff), t
+
+
+@pytest.mark.parametrize("nwarps", ["1", "8"])
+@pytest.mark.parametrize("tier", ["0", "1", "2", "3"])
+def test_every_layout_tier_and_warp_count(monkeypatch, nwarps, tier):
+    """The planner's shared-memory tiers (0 global, 1 group skeleton, 2 +chunk
+    skeleton, 3 +table) and the 8-warp variant give identical plans."""
+    from paper_1804_10001_b200.bestfit import solve_bestfit_arrays, solve_bestfit_batched_arrays
+    from paper_1804_10001_b200.workloads import uniform_arrays
+    import paper_1804_10001_b200 as mp
+    monkeypatch.setenv("MEMPLAN_NWARPS", nwarps)
+    monkeypatch.setenv("MEMPLAN_TIER", tier)
+    a, f, s = uniform_arrays(6000, 4)
+    s = ((s + 511) // 512) * 512
+    c = mp.profile_to_instance(mp.record(mp.parse_trace(mp.cnn_like_trace(
+        mp.GenSpec(model="cnn", layers=1500, seed=2)))), alignment=512).arrays()
+    for arr in ((a, f, s), c):
+        off, peak = solve_bestfit_arrays(*arr)
+        ooff, opeak = oracle.solve_bestfit(*arr)
+        assert peak == opeak and np.array_equal(off, ooff)
+    tp = np.array([0, 2000, 2001, 6000], np.int64)
+    off, peaks = solve_bestfit_batched_arrays(tp, a, f, s)
+    for t in range(3):
+        sl = slice(tp[t], tp[t + 1])
+        ooff, opeak = oracle.solve_bestfit(a[sl], f[sl], s[sl])
+        assert peaks[t] == opeak and np.array_equal(off[sl], ooff)
