@@ -339,7 +339,15 @@ __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint
                                            uint32_t rawhi, uint32_t lstar, uint32_t &best,
                                            uint32_t *pend, int &np, int lane);
 
-__device__ __forceinline__ void eval_loaded(const ChunkSk &c, int j, uint32_t thr,
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// PF: the table lives in global memory, so a segment that goes on the
+// pending list is prefetched into L2 right away (the drain reads it after
+// the remaining passes).
+template <bool PF>
+__device__ __forceinline__ void eval_loaded(const Win &w, const ChunkSk &c, int j, uint32_t thr,
                                             uint32_t rawhi, uint32_t lstar, uint32_t &best,
                                             uint32_t *pend, int &np, int lane) {
     bool need = false;
@@ -369,6 +377,10 @@ __device__ __forceinline__ void eval_loaded(const ChunkSk &c, int j, uint32_t th
                 if (pe < best && rawhi - q2.y >= lstar) {
                     need = true;
                     code = ((uint32_t)j << 2) | s;
+                    if (PF) {
+                        prefetch_l2(w.sf + 32 * j + 8 * s);
+                        prefetch_l2(w.sp + 32 * j + 8 * s);
+                    }
                 }
             }
         }
@@ -389,7 +401,7 @@ __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint
                                            uint32_t rawhi, uint32_t lstar, uint32_t &best,
                                            uint32_t *pend, int &np, int lane) {
     const ChunkSk c = load_chunk<SG>(w, j, valid);
-    eval_loaded(c, j, thr, rawhi, lstar, best, pend, np, lane);
+    eval_loaded<false>(w, c, j, thr, rawhi, lstar, best, pend, np, lane);
 }
 
 // Best contained block among the window chunks this warp handles (rule R4).
@@ -409,7 +421,10 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
     // left edge chunk (warp 0): issue the row read now, consume at the end
     bool edge = false;
     uint32_t ek = kNone, ep = kDead;
-    if (warp == 0 && partial) {  // speculative: no dependent skeleton check first
+    // the group skeleton (shared memory from tier GROUP up) says when nothing
+    // in the edge chunk's group fits at all: no row read, no chunk pass
+    const bool g0_fits = ldk<(TIER < TIER_GROUP)>(w.gs + (c0 >> 5), w.keep).x <= thr;
+    if (warp == 0 && partial && (TIER == TIER_ALL || g0_fits)) {  // speculative row read
         edge = true;
         ek = w.sf[32 * c0 + lane];
         ep = w.sp[32 * c0 + lane];
@@ -438,7 +453,9 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
     int gf = gcs;
     if (cs <= c1 && (cs & 31)) {
         gf = gcs + 1;
-        if (warp == 0) {
+        const bool gfits =
+            gcs == (c0 >> 5) ? g0_fits : ldk<(TIER < TIER_GROUP)>(w.gs + gcs, w.keep).x <= thr;
+        if (warp == 0 && gfits) {
             const int j = cs + lane;
             if (STATS) qs.pass++;
             eval_chunk<(TIER < TIER_SKEL)>(w, j, j <= c1 && j < 32 * gf, thr, rawhi, 0u, best,
@@ -504,7 +521,8 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
             for (int u = 0; u < kG; u++) {
                 if (__any_sync(kFull, jj[u] >= 0)) {
                     if (STATS) qs.pass++;
-                    eval_loaded(ck4[u], jj[u], thr, rawhi, lstar, best, pend, np, lane);
+                    eval_loaded<(TIER < TIER_ALL)>(w, ck4[u], jj[u], thr, rawhi, lstar, best,
+                                                   pend, np, lane);
                 }
             }
             if (np > kPendCap - 32 * kG) {
