@@ -359,6 +359,77 @@ __global__ void k_group_skel(const int64_t *__restrict__ trace_ptr, int64_t T,
     }
 }
 
+// Batch-wide key ranges for the composite-key sorts: [0] min alloc,
+// [1] max free, [2] max lifetime, [3] max size.
+__global__ void k_ranges(const int64_t *__restrict__ alloc, const int64_t *__restrict__ free_,
+                         const int64_t *__restrict__ size, int64_t N,
+                         unsigned long long *__restrict__ out) {
+    int64_t mn = INT64_MAX, mx = INT64_MIN, ml = 0, ms = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        mn = min(mn, alloc[i]);
+        mx = max(mx, free_[i]);
+        ml = max(ml, free_[i] - alloc[i]);
+        ms = max(ms, size[i]);
+    }
+    for (int o = 16; o; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+        ml = max(ml, __shfl_xor_sync(0xFFFFFFFFu, ml, o));
+        ms = max(ms, __shfl_xor_sync(0xFFFFFFFFu, ms, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        // order-preserving unsigned images of the signed values
+        atomicMin(out + 0, (unsigned long long)mn ^ 0x8000000000000000ull);
+        atomicMax(out + 1, (unsigned long long)mx ^ 0x8000000000000000ull);
+        atomicMax(out + 2, (unsigned long long)ml);
+        atomicMax(out + 3, (unsigned long long)ms);
+    }
+}
+
+// composite (trace, time - tmin) keys over alloc ∪ free; idx = iota
+__global__ void k_time_keys(const int64_t *__restrict__ alloc, const int64_t *__restrict__ free_,
+                            const uint32_t *__restrict__ tix, int64_t N, int64_t tmin, int tbits,
+                            uint64_t *__restrict__ keys, uint32_t *__restrict__ idx) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i < N ? i : i - N;
+        const int64_t t = i < N ? alloc[k] : free_[k];
+        keys[i] = ((uint64_t)tix[k] << tbits) | (uint64_t)(t - tmin);
+        idx[i] = (uint32_t)i;
+    }
+}
+
+// composite (trace, alloc rank) keys
+__global__ void k_arank_keys(const uint32_t *__restrict__ arank, const uint32_t *__restrict__ tix,
+                             int64_t N, int rbits, uint32_t *__restrict__ keys,
+                             uint32_t *__restrict__ vals) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = (tix[i] << rbits) | arank[i];
+        vals[i] = (uint32_t)i;
+    }
+}
+
+// composite (trace, lifetime desc, size desc) keys; ids ascend by stability
+__global__ void k_prio_keys(const int64_t *__restrict__ alloc, const int64_t *__restrict__ free_,
+                            const int64_t *__restrict__ size, const uint32_t *__restrict__ tix,
+                            int64_t N, int lbits, int sbits, uint64_t lmax, uint64_t smax,
+                            uint64_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t life = (uint64_t)(free_[i] - alloc[i]), sz = (uint64_t)size[i];
+        keys[i] = ((uint64_t)tix[i] << (lbits + sbits)) | ((lmax - life) << sbits) | (smax - sz);
+        vals[i] = (uint32_t)i;
+    }
+}
+
+inline int bits_for_u64(uint64_t v) {  // bits to hold 0..v
+    int b = 0;
+    while (b < 64 && (v >> b)) b++;
+    return b;
+}
+
 inline int bits_for(int64_t T) {
     int b = 1;
     while ((int64_t(1) << b) < T) b++;
@@ -442,13 +513,48 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
     k_trace_index<<<g1, kThreads, 0, s>>>(in.trace_ptr, T, tix, N);
     g_prep_k++;
 
+    // Large batches: one composite-key sort per ordering instead of a full
+    // 64-bit sort plus a stable regroup by trace, with the key widths cut to
+    // the batch's actual ranges (one small reduction + one host sync).
+    bool comp = false;
+    int tbits = 0, lbits = 0, sbits = 0;
+    uint64_t lmax = 0, smax = 0;
+    int64_t tmin = 0;
+    if (T > 1 && N >= (int64_t(1) << 16)) {
+        unsigned long long *rng = reinterpret_cast<unsigned long long *>(k64_s);
+        const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+        MP_CUDA(cudaMemcpyAsync(rng, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        k_ranges<<<std::min(g1, 148 * 8), kThreads, 0, s>>>(in.alloc, in.free_, in.size, N, rng);
+        g_prep_k++;
+        unsigned long long h[4];
+        MP_CUDA(cudaMemcpyAsync(h, rng, sizeof(h), cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        tmin = (int64_t)(h[0] ^ 0x8000000000000000ull);
+        const int64_t tmax = (int64_t)(h[1] ^ 0x8000000000000000ull);
+        const uint64_t span = (uint64_t)tmax - (uint64_t)tmin;
+        tbits = bits_for_u64(span);
+        lmax = h[2];
+        smax = h[3];
+        lbits = bits_for_u64(lmax);
+        sbits = bits_for_u64(smax);
+        comp = tb + tbits <= 64 && tb + lbits + sbits <= 64 && tmax >= tmin;
+    }
     // ---- compressed time ranks over alloc ∪ free, per trace ----
-    k_fill_times<<<g2, kThreads, 0, s>>>(in.alloc, in.free_, N, times, idx);
-    g_prep_k++;
     size_t tb_ = tbytes;
-    MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, times, times_s, idx, idx_s, (int)M, 0, 64, s));
     uint32_t *rk_idx = idx_s;
-    if (T > 1) {
+    if (comp) {
+        uint64_t *tk64 = reinterpret_cast<uint64_t *>(times), *tk64_s = reinterpret_cast<uint64_t *>(times_s);
+        k_time_keys<<<g2, kThreads, 0, s>>>(in.alloc, in.free_, tix, N, tmin, tbits, tk64, idx);
+        g_prep_k++;
+        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, tk64, tk64_s, idx, idx_s, (int)M, 0,
+                                                tb + tbits, s));
+    } else {
+        k_fill_times<<<g2, kThreads, 0, s>>>(in.alloc, in.free_, N, times, idx);
+        g_prep_k++;
+        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, times, times_s, idx, idx_s, (int)M, 0, 64,
+                                                s));
+    }
+    if (!comp && T > 1) {
         k_gather_tkey<<<g2, kThreads, 0, s>>>(idx_s, tix, N, M, tk);
         g_prep_k++;
         tb_ = tbytes;
@@ -467,12 +573,22 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
 
     // ---- (alloc, id) order: stable by alloc rank, then stable by trace ----
     uint32_t *ka = tk, *ka_s = tk_s, *va = idx, *va_s = idx_s;
-    k_iota_keys_arank<<<g1, kThreads, 0, s>>>(arank, N, ka, va);
-    g_prep_k++;
-    tb_ = tbytes;
-    MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, ka, ka_s, va, va_s, (int)N, 0, 32, s));
+    const int rbits = bits_for_u64((uint64_t)(2 * N + 2));  // ranks < 2n+1 per trace
+    const bool comp32 = comp && tb + rbits <= 32;
+    if (comp32) {
+        k_arank_keys<<<g1, kThreads, 0, s>>>(arank, tix, N, rbits, ka, va);
+        g_prep_k++;
+        tb_ = tbytes;
+        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, ka, ka_s, va, va_s, (int)N, 0,
+                                                tb + rbits, s));
+    } else {
+        k_iota_keys_arank<<<g1, kThreads, 0, s>>>(arank, N, ka, va);
+        g_prep_k++;
+        tb_ = tbytes;
+        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, ka, ka_s, va, va_s, (int)N, 0, 32, s));
+    }
     uint32_t *ord = va_s;
-    if (T > 1) {
+    if (!comp32 && T > 1) {
         k_gather_tix32<<<g1, kThreads, 0, s>>>(va_s, tix, N, ka);
         g_prep_k++;
         tb_ = tbytes;
@@ -487,6 +603,16 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
 
     // ---- priority order: stable size desc, then stable lifetime desc, then trace ----
     uint32_t *vp = idx, *vp_s = idx_s;
+    uint32_t *pord = nullptr;
+    if (comp) {
+        k_prio_keys<<<g1, kThreads, 0, s>>>(in.alloc, in.free_, in.size, tix, N, lbits, sbits, lmax,
+                                            smax, k64, vp);
+        g_prep_k++;
+        tb_ = tbytes;
+        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, k64, k64_s, vp, vp_s, (int)N, 0,
+                                                tb + lbits + sbits, s));
+        pord = vp_s;
+    } else {
     k_keys_size<<<g1, kThreads, 0, s>>>(in.size, N, k64, vp);
     g_prep_k++;
     tb_ = tbytes;
@@ -495,13 +621,14 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
     g_prep_k++;
     tb_ = tbytes;
     MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, k64, k64_s, vp_s, vp, (int)N, 0, 64, s));
-    uint32_t *pord = vp;
+    pord = vp;
     if (T > 1) {
         k_gather_tix32<<<g1, kThreads, 0, s>>>(vp, tix, N, tk);
         g_prep_k++;
         tb_ = tbytes;
         MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, tk, tk_s, vp, vp_s, (int)N, 0, tb, s));
         pord = vp_s;
+    }
     }
     k_inverse<<<g1, kThreads, 0, s>>>(pord, tix, in.trace_ptr, N, prio);
     g_prep_k++;

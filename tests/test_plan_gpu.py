@@ -161,3 +161,29 @@ def test_every_layout_tier_and_warp_count(monkeypatch, nwarps, tier):
         sl = slice(tp[t], tp[t + 1])
         ooff, opeak = oracle.solve_bestfit(a[sl], f[sl], s[sl])
         assert peaks[t] == opeak and np.array_equal(off[sl], ooff)
+
+
+def test_large_batch_composite_key_prep():
+    """Batches of >= 2^16 blocks take K0's composite-key sorts (one sort per
+    ordering, key widths cut to the batch's ranges); every trace must match."""
+    from paper_1804_10001_b200.bestfit import solve_bestfit_batched_arrays
+    from paper_1804_10001_b200.workloads import uniform_arrays
+    import paper_1804_10001_b200 as mp
+    cols = []
+    for i in range(6):
+        a, f, s = uniform_arrays(10000 + 37 * i, 300 + i)
+        cols.append((a + 1000 * i, f + 1000 * i, ((s + 511) // 512) * 512))
+    cols.append(mp.profile_to_instance(mp.record(mp.parse_trace(mp.cnn_like_trace(
+        mp.GenSpec(model="cnn", layers=6000, seed=5)))), alignment=512).arrays())
+    cols.append(tuple(np.zeros(0, np.int64) for _ in range(3)))
+    # equal raw times across traces and duplicate times inside one trace
+    cols.append((np.array([5, 5, 5, 7]), np.array([9, 6, 9, 9]), np.array([512, 1024, 512, 512])))
+    tp = np.zeros(len(cols) + 1, np.int64)
+    np.cumsum([len(c[0]) for c in cols], out=tp[1:])
+    assert tp[-1] >= 1 << 16
+    A = np.concatenate([c[0] for c in cols]); F = np.concatenate([c[1] for c in cols])
+    S = np.concatenate([c[2] for c in cols])
+    off, peaks = solve_bestfit_batched_arrays(tp, A, F, S)
+    for t, (a, f, s) in enumerate(cols):
+        ooff, opeak = oracle.solve_bestfit(a, f, s)
+        assert peaks[t] == opeak and np.array_equal(off[tp[t]:tp[t + 1]], ooff), t
