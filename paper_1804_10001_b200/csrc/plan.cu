@@ -57,6 +57,7 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kPendCap = 256;  // pending segment slots per warp (shared memory)
+constexpr int kG = 4;          // flagged groups evaluated per memory round
 
 // Shared-memory tiers for the window structures: nothing / group skeleton /
 // + chunk skeleton / + chunk-sorted table.
@@ -460,7 +461,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
             if (STATS) qs.pass++;
             eval_chunk<(TIER < TIER_SKEL)>(w, j, j <= c1 && j < 32 * gf, thr, rawhi, 0u, best,
                                             pend, np, lane);
-            if (np > kPendCap - 32 * 4) {
+            if (np > kPendCap - 32 * kG) {
                 if (STATS) qs.seg += np;
                 best = min(best, drain_pending(w, pend, np, thr, kNone, lane));
                 np = 0;
@@ -504,7 +505,6 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
         if (prune && __popc(m) >= 3) tighten();
         while (m) {
             // up to four flagged groups per memory round (left to right)
-            constexpr int kG = 4;
             ChunkSk ck4[kG];
             int jj[kG];
 #pragma unroll
