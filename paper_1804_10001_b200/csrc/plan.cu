@@ -61,7 +61,10 @@ constexpr int kG = 4;          // flagged groups evaluated per memory round
 
 // Shared-memory tiers for the window structures: nothing / group skeleton /
 // + chunk skeleton / + chunk-sorted table.
-enum { TIER_GLOBAL = 0, TIER_GROUP = 1, TIER_SKEL = 2, TIER_ALL = 3 };
+// TIER_SCAN: small traces keep the table in shared memory and scan their
+// (short) windows row by row — no skeletons to maintain at all.
+enum { TIER_GLOBAL = 0, TIER_GROUP = 1, TIER_SKEL = 2, TIER_ALL = 3, TIER_SCAN = 4 };
+constexpr int64_t kScanMaxBlocks = 4096;
 
 struct PlanArgs {
     const int64_t *trace_ptr;
@@ -214,7 +217,7 @@ struct RetireRow {
     uint4 gq;  // S0 of chunk 32*(j>>5) + lane (the retired chunk's group)
 };
 
-template <bool SG>
+template <bool SG, bool SCAN = false>
 __device__ __forceinline__ RetireRow retire_load(const Win &w, uint32_t pos, int lane) {
     RetireRow r;
     r.j = (int)(pos >> 5);
@@ -222,18 +225,19 @@ __device__ __forceinline__ RetireRow retire_load(const Win &w, uint32_t pos, int
     r.pr = w.sp[32 * r.j + lane];
     const int jj = (r.j & ~31) + lane;
     r.gq = make_uint4(kNone, kNone, kNone, 0u);
-    if (jj < w.nch) r.gq = ldk<SG>(w.s0 + jj, w.keep);
+    if (!SCAN && jj < w.nch) r.gq = ldk<SG>(w.s0 + jj, w.keep);
     return r;
 }
 
 // Mark the entry at (alloc,id)-position `pos` dead and rebuild its chunk's
-// skeleton (one warp).
-template <bool STATS>
+// skeleton (one warp; TIER_SCAN keeps no skeleton).
+template <bool STATS, bool SCAN = false>
 __device__ __forceinline__ void retire_finish(const Win &w, RetireRow r, uint32_t pos, int lane) {
     if ((r.key & 31u) == (pos & 31u) && r.key != kNone) {
         r.pr = kDead;
         w.sp[32 * r.j + lane] = kDead;
     }
+    if (SCAN) return;
     uint4 q;
     const uint32_t nlive = skel_store(r.key, r.pr, lane, w.s0, w.s1, w.s2, r.j, &q);
     if (STATS && lane == 0) w.cnt[r.j] = nlive;
@@ -408,6 +412,43 @@ __device__ __forceinline__ void eval_chunk(const Win &w, int j, bool valid, uint
 // Best contained block among the window chunks this warp handles (rule R4).
 // Returns the warp-wide minimum priority; `lbest` is this lane's candidate
 // and the lane holding the warp minimum has prefetched its record into r0/r1.
+// TIER_SCAN query: every chunk row of the window, four rows per round.
+template <bool STATS, int NW>
+__device__ __forceinline__ uint32_t query_scan(const Win &w, const uint4 *rec4, const uint2 *raw2,
+                                               int c0, int c1, uint32_t chi, uint32_t clop,
+                                               uint32_t chip, int warp, int lane,
+                                               uint32_t &lbest, uint4 &r0, uint4 &r1, uint2 &rw,
+                                               QStats &qs, bool rec_smem) {
+    const uint32_t thr = (chi << 5) | 31u;
+    uint32_t best = kNone;
+    for (int jb = c0 + 4 * warp; jb <= c1; jb += 4 * NW) {
+        uint32_t k[4], p[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int j = jb + u;
+            k[u] = kNone;
+            p[u] = kDead;
+            if (j <= c1) {
+                k[u] = w.sf[32 * j + lane];
+                p[u] = w.sp[32 * j + lane];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t pos = 32u * (uint32_t)(jb + u) + (k[u] & 31u);
+            if (pos >= clop && k[u] <= thr) best = min(best, p[u]);
+            if (STATS)
+                qs.wlive += __popc(__ballot_sync(kFull, k[u] != kNone && p[u] != kDead &&
+                                                            pos >= clop && pos < chip));
+        }
+        if (STATS) qs.pass++;
+    }
+    const uint32_t wb = __reduce_min_sync(kFull, best);
+    if (!rec_smem && best == wb && wb != kNone) load_rec(rec4, raw2, best, false, w.stream, r0, r1, rw);
+    lbest = best;
+    return wb;
+}
+
 template <bool STATS, int NW, int TIER>
 __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4, const uint2 *raw2,
                                                  uint32_t *pend, int c0, int c1, uint32_t chi,
@@ -415,6 +456,9 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
                                                  bool prune, int warp, int lane, uint32_t &lbest,
                                                  uint4 &r0, uint4 &r1, uint2 &rw, QStats &qs,
                                                  bool rec_smem) {
+    if constexpr (TIER == TIER_SCAN)
+        return query_scan<STATS, NW>(w, rec4, raw2, c0, c1, chi, clop, chip, warp, lane, lbest,
+                                     r0, r1, rw, qs, rec_smem);
     const uint32_t thr = (chi << 5) | 31u;
     uint32_t best = kNone;
     const bool partial = (clop & 31u) != 0;
@@ -604,7 +648,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     win.nch = nch;
     const int ngr = (nch + 31) >> 5;
     const int64_t gbase = group_base(base, t);
-    if (TIER >= TIER_GROUP) {
+    if (TIER >= TIER_GROUP && TIER != TIER_SCAN) {
         uint4 *g = reinterpret_cast<uint4 *>(smem + off);
         off += (size_t)ngr * 16;
         for (int i = threadIdx.x; i < ngr; i += 32 * NW) g[i] = a.gs[gbase + i];
@@ -612,7 +656,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     } else {
         win.gs = a.gs + gbase;
     }
-    if (TIER >= TIER_SKEL) {
+    if (TIER >= TIER_SKEL && TIER != TIER_SCAN) {
         uint4 *d = reinterpret_cast<uint4 *>(smem + off);
         off += (size_t)nch * 32 + align16((size_t)nch * 8);
         for (int i = threadIdx.x; i < nch; i += 32 * NW) {
@@ -628,7 +672,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         win.s1 = a.s1 + cb;
         win.s2 = a.s2 + cb;
     }
-    if (TIER == TIER_ALL) {
+    if (TIER == TIER_ALL || TIER == TIER_SCAN) {
         uint32_t *d = reinterpret_cast<uint32_t *>(smem + off);
         off += (size_t)nch * 32 * 8;
         const uint4 *s0 = reinterpret_cast<const uint4 *>(a.sf + 32 * cb);
@@ -794,8 +838,9 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
                 // the winning warp retires the entry while the leader
                 // rewrites the skyline (both finish before barrier [A])
                 const uint32_t pos = r0.x;
-                retire_finish<STATS>(win, retire_load<(TIER < TIER_SKEL)>(win, pos, lane), pos,
-                                     lane);
+                retire_finish<STATS, TIER == TIER_SCAN>(
+                    win, retire_load<(TIER < TIER_SKEL), TIER == TIER_SCAN>(win, pos, lane), pos,
+                    lane);
             }
             if (warp != 0) continue;
         } else {
@@ -845,7 +890,8 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
             // place (R6)
             const uint32_t rpos = r0.x, rar = r0.y, rfr = r0.z, rap = r0.w, rfp = r1.x,
                            rk = r1.y;
-            if (NW == 1) rr = retire_load<(TIER < TIER_SKEL)>(win, rpos, lane);  // overlaps the update
+            if (NW == 1)  // the row read overlaps the skyline update
+                rr = retire_load<(TIER < TIER_SKEL), TIER == TIER_SCAN>(win, rpos, lane);
             HT rsz = (HT)r1.z;
             if (sizeof(HT) == 8) rsz |= (HT)((uint64_t)r1.w << 32);
             const HT ch = KO::h(ck);
@@ -923,7 +969,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         maxl = max(maxl, nl);
         c = cnext;
         if (TIMING) { const long long t2 = clock64(); tph[2] += t2 - tc; tc = t2; }
-        if (NW == 1 && gbest != kNone) retire_finish<STATS>(win, rr, r0.x, lane);
+        if (NW == 1 && gbest != kNone) retire_finish<STATS, TIER == TIER_SCAN>(win, rr, r0.x, lane);
         __syncwarp();
         if (TIMING) {
             const long long t2 = clock64();
@@ -997,6 +1043,7 @@ int launch_nw(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
 template <typename HT, bool Ls, bool ST>
 int launch_tier(const PlanArgs &a, int grid, int tier, size_t smem, cudaStream_t s) {
     switch (tier) {
+        case TIER_SCAN: return launch_nw<HT, Ls, ST, TIER_SCAN>(a, grid, smem, s);
         case TIER_ALL: return launch_nw<HT, Ls, ST, TIER_ALL>(a, grid, smem, s);
         case TIER_SKEL: return launch_nw<HT, Ls, ST, TIER_SKEL>(a, grid, smem, s);
         case TIER_GROUP: return launch_nw<HT, Ls, ST, TIER_GROUP>(a, grid, smem, s);
@@ -1045,7 +1092,7 @@ size_t lines_bytes(int lcap, size_t hbytes) {
 }
 
 Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwarps,
-                     bool force_global, bool lines_global = false, int max_tier = TIER_ALL) {
+                     bool force_global, bool lines_global = false, int max_tier = TIER_SCAN) {
     Layout l{};
     l.tier = TIER_GLOBAL;
     const size_t lines_b = lines_bytes(lcap, hbytes);
@@ -1073,6 +1120,21 @@ Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwar
         }
     }
     l.smem = used;
+    // small traces: table + records in shared memory, no skeletons (scan)
+    int64_t scan_max = kScanMaxBlocks;
+    if (const char *env = getenv("MEMPLAN_SCAN_MAX")) scan_max = atoll(env);  // tuning
+    if (!force_global && max_tier >= TIER_SCAN && nmax <= scan_max) {
+        size_t u2 = pend_b + (l.lines_smem ? lines_b : 0);
+        if (u2 + tab_b <= lim) {
+            Layout sc = l;
+            sc.tier = TIER_SCAN;
+            u2 += tab_b;
+            sc.rec_smem = u2 + rec_b <= lim;
+            if (sc.rec_smem) u2 += rec_b;
+            sc.smem = u2;
+            return sc;
+        }
+    }
     return l;
 }
 
@@ -1271,9 +1333,12 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     g_info.plan_ms = ms_plan;
     g_info.kernel_ms = ms_kernel;
     g_info.launches = prep_launches() + (g_launches - launches0);
-    g_info.engine = (h32 ? 16 : 0) | (lay.lines_smem ? 8 : 0) | (lay.tier >= TIER_SKEL ? 4 : 0) |
-                    (lay.tier == TIER_ALL ? 2 : 0) | (lay.rec_smem ? 1 : 0) |
-                    (redo.empty() ? 0 : 32) | (lay.tier >= TIER_GROUP ? 64 : 0);
+    g_info.engine = (h32 ? 16 : 0) | (lay.lines_smem ? 8 : 0) |
+                    (lay.tier >= TIER_SKEL && lay.tier != TIER_SCAN ? 4 : 0) |
+                    (lay.tier >= TIER_ALL ? 2 : 0) | (lay.rec_smem ? 1 : 0) |
+                    (redo.empty() ? 0 : 32) |
+                    (lay.tier >= TIER_GROUP && lay.tier != TIER_SCAN ? 64 : 0) |
+                    (lay.tier == TIER_SCAN ? 128 : 0);
     g_info.cluster = g_nwarps;  // warps per trace (single-CTA engine)
     for (int64_t t = 0; t < T; t++) {
         g_info.steps += hst[t * ST_N + ST_STEPS];

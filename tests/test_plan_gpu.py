@@ -138,7 +138,7 @@ def test_large_batch_mixed_sizes():
 
 
 @pytest.mark.parametrize("nwarps", ["1", "8"])
-@pytest.mark.parametrize("tier", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("tier", ["0", "1", "2", "3", "4"])
 def test_every_layout_tier_and_warp_count(monkeypatch, nwarps, tier):
     """The planner's shared-memory tiers (0 global, 1 group skeleton, 2 +chunk
     skeleton, 3 +table) and the 8-warp variant give identical plans."""
