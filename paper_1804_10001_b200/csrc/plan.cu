@@ -4,36 +4,38 @@
 // (bestfit.py:61-201) and _RemainingBlocks.take_best (bestfit.py:243-262).
 // Output is bit-identical to the reference: same offset per id, same peak.
 //
-// One CTA owns one trace and runs the reference's dependent step loop.
+// One CTA (normally one warp) owns one trace and runs the reference's
+// dependent step loop; a batch launches one CTA per trace.
 //
 //  skyline   lines kept as a compact, time-sorted array: line i spans
 //            [LO[i], LO[i+1]) at height H[i]; LOP[i] is the first (alloc,id)
-//            position with alloc >= LO[i].  A sentinel at index L holds
-//            (t_hi, n).  Heights are in units of the trace's size gcd, so for
-//            all realistic traces they fit 32 bits and (H, LO) packs into one
-//            u64 argmin key.
+//            position with alloc >= LO[i]; RAW[i] is LO's raw time.  A
+//            sentinel at index L holds (t_hi, n).  Heights are in units of the
+//            trace's size gcd, so for realistic traces they fit 32 bits and
+//            (H, LO) packs into one u64 argmin key.
 //  choose    rule R3 (bestfit.py:115-122): warp argmin of (height, lo).
 //            Skipped after a placement that leaves a shoulder (the shoulder
 //            is the new lowest-leftmost line).
 //  query     rule R4 (bestfit.py:243-256): the window is positions
 //            [LOP[c], LOP[c+1]); a block fits iff its free rank <= hi.  Whole
-//            chunks are answered from the shared-memory chunk skeleton
-//            (plan_types.cuh): none fits / the chunk's best entry fits ->
-//            exact answer; otherwise the skeleton names the one 8-slot
-//            segment where the fitting prefix ends, and that segment is
-//            read from the table (two 32-byte sectors) only if its prefix
-//            minimum can still beat the lane's best.  All such segment reads
-//            of a step are issued together (one memory round), overlapped
-//            with the prefetch of the provisional winner's record.  The
-//            partial left chunk is read as one row.  Winner = minimum
-//            priority rank = max (lifetime, size, -id).
+//            groups of 32 chunks, then chunks, are answered from skeletons
+//            (plan_types.cuh): nothing fits / the best entry fits -> exact;
+//            otherwise a chunk's skeleton names the one 8-slot segment where
+//            its fitting prefix ends, and that segment is read from the table
+//            only if its prefix minimum can still beat the best so far.
+//            Lifetime bounds (priority is lifetime-major; a block of a group
+//            or chunk that fits lives at most raw(hi) - its raw alloc
+//            origin) skip groups and segments that cannot win.  Winner =
+//            minimum priority rank = max (lifetime, size, -id).  Traces of
+//            at most kScanMaxBlocks blocks (TIER_SCAN) scan their window rows
+//            from shared memory instead and keep no skeletons.
 //  update    place (R6, :149-178) and lift_up (R5, :180-201) both replace
 //            the chosen line (and at most one right neighbour) by <= 3 lines;
 //            the tail shifts by d in [-2, 2] with warp-parallel copies.  The
-//            winner's table slot is retired and its chunk skeleton rebuilt
-//            (one row read, overlapped with the skyline update).
+//            winner's table slot is retired and its chunk and group
+//            skeletons rebuilt (one row read, overlapped with the update).
 //
-// NW = 1: one warp, no block barriers at all.  NW > 1: warp 0 leads
+// NW = 1: one warp, no block barriers at all.  NW > 1 (tuning): warp 0 leads
 // (choose + update), all warps split the window; two barriers per step.
 //
 // The loop bound assert (R8, bestfit.py:297) and IllegalLift (:185-186)
