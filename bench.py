@@ -289,7 +289,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("MEMPLAN_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
     lib = N.lib()
@@ -346,10 +350,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        return float(t.item())
+
+    ms = max_over_ranks(ms)
     value = world * NB / (ms / 1e3)
 
     # e2e: public C ABI with pinned host buffers (H2D + D2H inside the region)
@@ -370,11 +378,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_each.append(e0.elapsed_time(e1))
-    e2e_ms = float(np.median(e2e_each))
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(float(np.median(e2e_each)))
     e2e_value = world * NB / (e2e_ms / 1e3)
 
     # single-trace latency (one trace of the same family, device pointers)
@@ -488,7 +492,8 @@ def main():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=100_000)
+    p.add_argument("--blocks", dest="n", type=int, default=100_000,
+                   help="blocks per trace (not --n: torchrun would take it as its own flag)")
     p.add_argument("--traces", type=int, default=1184)
     p.add_argument("--cpu-procs", type=int, default=32)
     p.add_argument("--no-cpu", action="store_true")
@@ -502,6 +507,10 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", args.gpus))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    # test hook: run every rank on one device (functional check of the N > 1
+    # path on a single GPU, with MEMPLAN_BENCH_BACKEND=gloo)
+    if os.environ.get("MEMPLAN_BENCH_DEVICE") is not None:
+        local_rank = int(os.environ["MEMPLAN_BENCH_DEVICE"])
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

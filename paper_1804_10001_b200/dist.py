@@ -130,6 +130,9 @@ def gather_device(local_traces, d_offsets, d_peaks):
 
     world, rank = dist.get_world_size(), dist.get_rank()
     dev = d_offsets.device
+    if dist.get_backend() != "nccl":  # gloo moves host tensors
+        dev = torch.device("cpu")
+        d_offsets, d_peaks = d_offsets.cpu(), d_peaks.cpu()
     ids = torch.as_tensor(local_traces, dtype=torch.int64, device=dev)
     payload = torch.cat([ids, d_peaks.to(torch.int64), d_offsets.to(torch.int64)])
     n = torch.tensor([payload.numel()], dtype=torch.int64, device=dev)
