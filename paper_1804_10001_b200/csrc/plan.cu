@@ -51,6 +51,7 @@
 #include "plan.h"
 #include "plan_types.cuh"
 #include "prep.h"
+#include "fused_prep.cuh"
 
 namespace mp {
 
@@ -604,8 +605,10 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
     return wb;
 }
 
+// The step loop for trace t, run by threads [0, 32*NW) of the CTA (k_plan
+// launches exactly those; the fused small-trace kernel hands its warp 0 in).
 template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER, bool TIMING>
-__global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
+__device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
     using KO = KeyT<HT>;
     using K = typename KO::K;
     using LR = LineRec<K>;
@@ -613,7 +616,6 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     __shared__ StepShared<K> ss;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int t = a.tlist ? a.tlist[blockIdx.x] : (int)blockIdx.x;
     const int64_t base = a.trace_ptr[t];
     const int n = (int)(a.trace_ptr[t + 1] - base);
     int64_t *st = a.stats + (int64_t)t * ST_N;
@@ -709,7 +711,8 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
         L[1].raw = prune ? (uint32_t)a.tspan[t] : 0u;
         ss.done = 0;
     }
-    __syncthreads();
+    if (NW > 1) __syncthreads();
+    else __syncwarp();
 
     // leader-warp state (warp 0; uniform across its lanes)
     int nl = 1;
@@ -1007,6 +1010,31 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     }
 }
 
+template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER, bool TIMING>
+__global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
+    plan_trace<HT, LINES_SMEM, STATS, NW, TIER, TIMING>(a, a.tlist ? a.tlist[blockIdx.x]
+                                                                   : (int)blockIdx.x);
+}
+
+// Fused small-trace path: one CTA per trace runs K0 for its trace in shared
+// memory (prep_small), then its warp 0 runs the TIER_SCAN step loop.
+template <int ITEMS, bool STATS>
+__global__ void __launch_bounds__(kFusedThreads) k_fused_small(PlanArgs a, FusedIn in) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int t = (int)blockIdx.x;
+    const int64_t n = a.trace_ptr[t + 1] - a.trace_ptr[t];
+    if (n > 0)
+        prep_small<ITEMS>(a.trace_ptr, in, a.sf, a.sp, const_cast<Rec *>(a.rec),
+                          const_cast<uint2 *>(a.raw2), t, smem);
+    if (threadIdx.x >= 32) return;
+    if (n == 0 || in.total_units[t] < (uint64_t(1) << 32))
+        plan_trace<uint32_t, true, STATS, 1, TIER_SCAN, false>(a, t);
+    else
+        plan_trace<uint64_t, true, STATS, 1, TIER_SCAN, false>(a, t);
+}
+
+constexpr int64_t kFusedMaxBlocks = 2048;
+
 thread_local int64_t g_launches = 0;
 thread_local int g_nwarps = 1;  // warps per trace chosen by plan_device
 thread_local int g_carveout = -1;  // shared-memory carveout percent (-1: driver default)
@@ -1144,6 +1172,139 @@ Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwar
 
 const mp_plan_info &last_plan_info() { return g_info; }
 
+namespace {
+
+// Fold per-trace planner statistics into g_info; map the status words to the
+// reference's errors.
+int collect_stats(const std::vector<int64_t> &hst, int64_t T) {
+    for (int64_t t = 0; t < T; t++) {
+        g_info.steps += hst[t * ST_N + ST_STEPS];
+        g_info.lifts += hst[t * ST_N + ST_LIFTS];
+        g_info.sum_wlive += hst[t * ST_N + ST_WLIVE];
+        for (int k = 0; k < 4; k++) g_info.diag[k] += hst[t * ST_N + ST_SCAN + k];
+        for (int k = 0; k < 6; k++) g_info.cycles[k] += hst[t * ST_N + ST_T0 + k];
+        g_info.max_lines = std::max(g_info.max_lines, hst[t * ST_N + ST_MAXLINES]);
+        const int64_t stv = hst[t * ST_N + ST_STATUS];
+        if (stv == PS_LOOP_BOUND) {
+            set_error("best-fit loop exceeded its iteration bound");
+            return MP_ERR_LOOP_BOUND;
+        }
+        if (stv == PS_ILLEGAL_LIFT) {
+            set_error("cannot lift the only offset line");
+            return MP_ERR_ILLEGAL_LIFT;
+        }
+        if (stv != PS_OK) {
+            set_error("planner status " + std::to_string(stv));
+            return MP_ERR_CUDA;
+        }
+    }
+    return MP_OK;
+}
+
+constexpr int kFusedFallback = -1;
+
+template <int ITEMS>
+int launch_fused(const PlanArgs &a, const FusedIn &in, int grid, size_t smem, bool stats,
+                 cudaStream_t s) {
+    auto fn = stats ? k_fused_small<ITEMS, true> : k_fused_small<ITEMS, false>;
+    MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<grid, kFusedThreads, smem, s>>>(a, in);
+    MP_CUDA(cudaGetLastError());
+    g_launches++;
+    return MP_OK;
+}
+
+// Traces of at most kFusedMaxBlocks blocks: one launch, no global sorts and
+// no host round trip between K0 and the planner.  Returns kFusedFallback
+// when the batch is not eligible or a skyline outgrew shared memory (the
+// caller then takes the general path, which restarts such traces).
+int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
+               const int64_t *alloc_d, const int64_t *free_d, const int64_t *size_d,
+               int64_t *offsets_d, int64_t *peaks_d, int flags, int device, cudaStream_t s) {
+    if (nmax > kFusedMaxBlocks || (flags & MP_FORCE_GLOBAL) || getenv("MEMPLAN_NO_FUSED"))
+        return kFusedFallback;
+    const int items = nmax <= 256 ? 2 : (nmax <= 512 ? 4 : 16);
+    const size_t prep_smem = items == 2 ? sizeof(SmallPrep<2>::Shared)
+                            : items == 4 ? sizeof(SmallPrep<4>::Shared)
+                                         : sizeof(SmallPrep<16>::Shared);
+    // planner layout (TIER_SCAN), sized for 64-bit heights so either fits
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const size_t lim = smem_limit(device) - 8192;  // two StepShared blocks + prep statics
+    const int conc = (int)std::min<int64_t>((T + sms - 1) / sms, 8);
+    const size_t budget = conc > 1 ? std::min(lim, (size_t)(228 * 1024) / conc - 8192) : lim;
+    const int64_t lneed = 2 * nmax + 2;
+    const int lcap = (int)std::min<int64_t>(lneed, conc > 1 ? 256 : 1024);
+    Layout lay = choose_layout(nmax, lcap, 8, budget, 1, false);
+    if (lay.tier != TIER_SCAN || !lay.lines_smem) return kFusedFallback;
+    const size_t smem = std::max(prep_smem + 256, lay.smem);
+    if (smem > lim) return kFusedFallback;
+
+    const int64_t nchunks = N / 32 + T + 1;
+    const size_t bytes = 2 * Carver::need<uint32_t>(32 * nchunks) + Carver::need<Rec>(N) +
+                         Carver::need<uint2>(N) + Carver::need<uint32_t>(T) +
+                         4 * Carver::need<int64_t>(T) + Carver::need<int64_t>(T * ST_N);
+    Scratch sc;
+    MP_TRY(sc.alloc(bytes, s));
+    Carver cv(sc.ptr, bytes);
+    PlanArgs a{};
+    FusedIn in{};
+    a.trace_ptr = trace_ptr_d;
+    a.sf = cv.take<uint32_t>(32 * nchunks);
+    a.sp = cv.take<uint32_t>(32 * nchunks);
+    Rec *rec = cv.take<Rec>(N);
+    uint2 *raw2 = cv.take<uint2>(N);
+    a.rec = rec;
+    a.raw2 = raw2;
+    in.U = cv.take<uint32_t>(T);
+    in.unit = cv.take<int64_t>(T);
+    in.tmin = cv.take<int64_t>(T);
+    in.tspan = cv.take<int64_t>(T);
+    in.total_units = reinterpret_cast<uint64_t *>(cv.take<int64_t>(T));
+    int64_t *stats = cv.take<int64_t>(T * ST_N);
+    in.alloc = alloc_d;
+    in.free_ = free_d;
+    in.size = size_d;
+    a.U = in.U;
+    a.unit = in.unit;
+    a.tspan = in.tspan;
+    a.offsets = offsets_d;
+    a.peaks = peaks_d;
+    a.stats = stats;
+    a.lcap = lcap;
+    a.rec_smem = lay.rec_smem;
+    const bool stats_on = (flags & MP_STATS) != 0;
+    cudaEvent_t k0, k1;
+    cudaEventCreate(&k0);
+    cudaEventCreate(&k1);
+    const int64_t launches0 = g_launches;
+    cudaEventRecord(k0, s);
+    int rc = items == 2 ? launch_fused<2>(a, in, (int)T, smem, stats_on, s)
+           : items == 4 ? launch_fused<4>(a, in, (int)T, smem, stats_on, s)
+                        : launch_fused<16>(a, in, (int)T, smem, stats_on, s);
+    if (rc != MP_OK) return rc;
+    cudaEventRecord(k1, s);
+    std::vector<int64_t> hst((size_t)T * ST_N);
+    MP_CUDA(cudaMemcpyAsync(hst.data(), stats, sizeof(int64_t) * T * ST_N,
+                            cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    for (int64_t t = 0; t < T; t++)
+        if (hst[t * ST_N + ST_STATUS] == PS_LINES_OVERFLOW) return kFusedFallback;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, k0, k1);
+    cudaEventDestroy(k0);
+    cudaEventDestroy(k1);
+    g_info.prep_ms = 0;
+    g_info.plan_ms = ms;
+    g_info.kernel_ms = ms;
+    g_info.launches = g_launches - launches0;
+    g_info.engine = 8 | 2 | (lay.rec_smem ? 1 : 0) | 128 | 256;  // 256: fused small-trace path
+    g_info.cluster = 1;
+    return collect_stats(hst, T);
+}
+
+}  // namespace
+
 int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t T,
                 const int64_t *alloc_d, const int64_t *free_d, const int64_t *size_d,
                 int64_t *offsets_d, int64_t *peaks_d, int flags, int device, cudaStream_t s) {
@@ -1159,6 +1320,12 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     if (2 * nmax + 2 >= (int64_t(1) << kRankBits)) {
         set_error("trace too large (free ranks must fit 27 bits: n < 2^26)");
         return MP_ERR_INVALID;
+    }
+    {
+        const int rc = plan_fused(trace_ptr_d, T, N, nmax, alloc_d, free_d, size_d, offsets_d,
+                                  peaks_d, flags, device, s);
+        if (rc != kFusedFallback) return rc;
+        g_info = mp_plan_info{};
     }
     const int64_t nchunks = N / 32 + T + 1;
     const int64_t ngroups = nchunks / 32 + T + 1;
@@ -1342,28 +1509,7 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
                     (lay.tier >= TIER_GROUP && lay.tier != TIER_SCAN ? 64 : 0) |
                     (lay.tier == TIER_SCAN ? 128 : 0);
     g_info.cluster = g_nwarps;  // warps per trace (single-CTA engine)
-    for (int64_t t = 0; t < T; t++) {
-        g_info.steps += hst[t * ST_N + ST_STEPS];
-        g_info.lifts += hst[t * ST_N + ST_LIFTS];
-        g_info.sum_wlive += hst[t * ST_N + ST_WLIVE];
-        for (int k = 0; k < 4; k++) g_info.diag[k] += hst[t * ST_N + ST_SCAN + k];
-        for (int k = 0; k < 6; k++) g_info.cycles[k] += hst[t * ST_N + ST_T0 + k];
-        g_info.max_lines = std::max(g_info.max_lines, hst[t * ST_N + ST_MAXLINES]);
-        int64_t stv = hst[t * ST_N + ST_STATUS];
-        if (stv == PS_LOOP_BOUND) {
-            set_error("best-fit loop exceeded its iteration bound");
-            return MP_ERR_LOOP_BOUND;
-        }
-        if (stv == PS_ILLEGAL_LIFT) {
-            set_error("cannot lift the only offset line");
-            return MP_ERR_ILLEGAL_LIFT;
-        }
-        if (stv != PS_OK) {
-            set_error("planner status " + std::to_string(stv));
-            return MP_ERR_CUDA;
-        }
-    }
-    return MP_OK;
+    return collect_stats(hst, T);
 }
 
 }  // namespace mp
