@@ -14,7 +14,7 @@
 
 namespace mp {
 
-constexpr int kFusedThreads = 256;
+constexpr int kFusedMaxThreads = 256;
 
 struct FusedIn {
     const int64_t *alloc, *free_, *size;  // batch columns (device)
@@ -34,31 +34,31 @@ __device__ __forceinline__ int64_t gcd64f(int64_t a, int64_t b) {
 
 __device__ __forceinline__ int bits_u64(uint64_t v) { return v ? 64 - __clzll((long long)v) : 0; }
 
-// Shared-memory footprint of prep_small<ITEMS> for traces of at most
-// kFusedThreads * ITEMS / 2 blocks.
-template <int ITEMS> struct SmallPrep {
-    static constexpr int C = kFusedThreads * ITEMS;  // sort capacity (2n)
+// Shared-memory footprint of prep_small<THREADS, ITEMS> for traces of at
+// most THREADS * ITEMS / 2 blocks.
+template <int THREADS, int ITEMS> struct SmallPrep {
+    static constexpr int C = THREADS * ITEMS;  // sort capacity (2n)
     static constexpr int NMAX = C / 2;
-    using SortT = cub::BlockRadixSort<uint64_t, kFusedThreads, ITEMS, uint32_t>;
-    using ScanT = cub::BlockScan<uint32_t, kFusedThreads>;
+    using SortT = cub::BlockRadixSort<uint64_t, THREADS, ITEMS, uint32_t>;
+    using ScanT = cub::BlockScan<uint32_t, THREADS>;
     union Temp {
         typename SortT::TempStorage sort;
         typename ScanT::TempStorage scan;
     };
     struct Shared {
         Temp temp;
-        uint64_t last_key[kFusedThreads];
-        int64_t red[4][kFusedThreads / 32];
+        uint64_t last_key[THREADS];
         uint32_t arank[NMAX], frank[NMAX], posof[NMAX], sar[NMAX], prio[NMAX];
         uint2 ent[NMAX];
         uint32_t U;
     };
 };
 
-template <int ITEMS>
+template <int THREADS, int ITEMS>
 __device__ void prep_small(const int64_t *trace_ptr, const FusedIn &in, uint32_t *sf, uint32_t *sp,
                            Rec *rec, uint2 *raw2, int t, unsigned char *smem_raw) {
-    using P = SmallPrep<ITEMS>;
+    using P = SmallPrep<THREADS, ITEMS>;
+    constexpr int NWARP = THREADS / 32;
     typename P::Shared &sh = *reinterpret_cast<typename P::Shared *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t b = trace_ptr[t];
@@ -67,7 +67,7 @@ __device__ void prep_small(const int64_t *trace_ptr, const FusedIn &in, uint32_t
 
     // ---- ranges, gcd (trace scalars; k_trace_scale in prep.cu) ----
     int64_t mn = INT64_MAX, mx = INT64_MIN, g = 0, lm = 0, sm = 0;
-    for (int i = tid; i < n; i += kFusedThreads) {
+    for (int i = tid; i < n; i += THREADS) {
         mn = min(mn, A[i]);
         mx = max(mx, F[i]);
         g = gcd64f(S[i], g);
@@ -81,14 +81,14 @@ __device__ void prep_small(const int64_t *trace_ptr, const FusedIn &in, uint32_t
         lm = max(lm, __shfl_xor_sync(0xFFFFFFFFu, lm, o));
         sm = max(sm, __shfl_xor_sync(0xFFFFFFFFu, sm, o));
     }
-    __shared__ int64_t red5[5][kFusedThreads / 32];
+    __shared__ int64_t red5[5][NWARP];
     if (lane == 0) {
         red5[0][warp] = mn; red5[1][warp] = mx; red5[2][warp] = g;
         red5[3][warp] = lm; red5[4][warp] = sm;
     }
     __syncthreads();
     mn = red5[0][0]; mx = red5[1][0]; g = red5[2][0]; lm = red5[3][0]; sm = red5[4][0];
-    for (int w = 1; w < kFusedThreads / 32; w++) {
+    for (int w = 1; w < NWARP; w++) {
         mn = min(mn, red5[0][w]); mx = max(mx, red5[1][w]); g = gcd64f(g, red5[2][w]);
         lm = max(lm, red5[3][w]); sm = max(sm, red5[4][w]);
     }
@@ -98,7 +98,7 @@ __device__ void prep_small(const int64_t *trace_ptr, const FusedIn &in, uint32_t
     // total size in units of g, saturating at 2^62 (selects the height width)
     const uint64_t cap = uint64_t(1) << 62;
     uint64_t acc = 0;
-    for (int i = tid; i < n; i += kFusedThreads) {
+    for (int i = tid; i < n; i += THREADS) {
         acc += (uint64_t)(S[i] / g);
         if (acc > cap) acc = cap;
     }
@@ -111,7 +111,7 @@ __device__ void prep_small(const int64_t *trace_ptr, const FusedIn &in, uint32_t
     __syncthreads();
     if (tid == 0) {
         uint64_t tot = 0;
-        for (int w = 0; w < kFusedThreads / 32; w++) {
+        for (int w = 0; w < NWARP; w++) {
             tot += (uint64_t)red5[0][w];
             if (tot > cap) tot = cap;
         }
@@ -203,7 +203,7 @@ __device__ void prep_small(const int64_t *trace_ptr, const FusedIn &in, uint32_t
     __syncthreads();
 
     // ---- records, raw times, window entries ----
-    for (int i = tid; i < n; i += kFusedThreads) {
+    for (int i = tid; i < n; i += THREADS) {
         Rec r;
         r.pos = sh.posof[i];
         r.arank = sh.arank[i];
@@ -233,7 +233,7 @@ __device__ void prep_small(const int64_t *trace_ptr, const FusedIn &in, uint32_t
     // ---- chunk-sorted table rows (k_chunk_sort without skeletons) ----
     const int64_t cb = chunk_base(b, t);
     const int nch = (n + 31) >> 5;
-    for (int j = warp; j < nch; j += kFusedThreads / 32) {
+    for (int j = warp; j < nch; j += NWARP) {
         const int p = 32 * j + lane;
         uint32_t k = 0xFFFFFFFFu, pr = kDead;
         if (p < n) {

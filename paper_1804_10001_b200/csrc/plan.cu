@@ -1018,13 +1018,13 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
 
 // Fused small-trace path: one CTA per trace runs K0 for its trace in shared
 // memory (prep_small), then its warp 0 runs the TIER_SCAN step loop.
-template <int ITEMS, bool STATS>
-__global__ void __launch_bounds__(kFusedThreads) k_fused_small(PlanArgs a, FusedIn in) {
+template <int THREADS, int ITEMS, bool STATS>
+__global__ void __launch_bounds__(THREADS) k_fused_small(PlanArgs a, FusedIn in) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int t = (int)blockIdx.x;
     const int64_t n = a.trace_ptr[t + 1] - a.trace_ptr[t];
     if (n > 0)
-        prep_small<ITEMS>(a.trace_ptr, in, a.sf, a.sp, const_cast<Rec *>(a.rec),
+        prep_small<THREADS, ITEMS>(a.trace_ptr, in, a.sf, a.sp, const_cast<Rec *>(a.rec),
                           const_cast<uint2 *>(a.raw2), t, smem);
     if (threadIdx.x >= 32) return;
     if (n == 0 || in.total_units[t] < (uint64_t(1) << 32))
@@ -1034,6 +1034,49 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_small(PlanArgs a, Fused
 }
 
 constexpr int64_t kFusedMaxBlocks = 2048;
+
+// Per-trace stats rows -> one row, on the device, so a batch of thousands of
+// small traces returns 8 * (ST_N + 2) bytes instead of 8 * ST_N per trace.
+// out[ST_STATUS] is the status of the first trace (in batch order) that
+// failed with anything but a skyline overflow, out[ST_N] counts overflowed
+// traces, out[ST_N + 1] is that first failing trace (or T).
+constexpr int kRedThreads = 256;
+__global__ void __launch_bounds__(kRedThreads) k_reduce_stats(const int64_t *st, int64_t T,
+                                                              int64_t *out) {
+    __shared__ int64_t part[kRedThreads];
+    int64_t acc[ST_N], ovf = 0, first = T;
+#pragma unroll
+    for (int k = 0; k < ST_N; k++) acc[k] = 0;
+    for (int64_t t = threadIdx.x; t < T; t += kRedThreads) {
+        const int64_t *row = st + t * ST_N;
+#pragma unroll
+        for (int k = 0; k < ST_N; k++)
+            if (k == ST_MAXLINES) acc[k] = max(acc[k], row[k]);
+            else if (k != ST_STATUS) acc[k] += row[k];
+        const int64_t stv = row[ST_STATUS];
+        if (stv == PS_LINES_OVERFLOW) ovf++;
+        else if (stv != PS_OK && t < first) first = t;
+    }
+    // one slot at a time through shared memory (ST_N + 2 small reductions)
+    for (int k = 0; k < ST_N + 2; k++) {
+        const int64_t v = k < ST_N ? acc[k] : (k == ST_N ? ovf : first);
+        part[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = kRedThreads / 2; o; o >>= 1) {
+            if ((int)threadIdx.x < o) {
+                const int64_t x = part[threadIdx.x], y = part[threadIdx.x + o];
+                part[threadIdx.x] = (k == ST_MAXLINES) ? max(x, y)
+                                  : (k == ST_N + 1)    ? min(x, y)
+                                                       : x + y;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[k] = part[0];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[ST_STATUS] = out[ST_N + 1] < T ? st[out[ST_N + 1] * ST_N + ST_STATUS]
+                                                             : PS_OK;
+}
 
 thread_local int64_t g_launches = 0;
 thread_local int g_nwarps = 1;  // warps per trace chosen by plan_device
@@ -1203,12 +1246,12 @@ int collect_stats(const std::vector<int64_t> &hst, int64_t T) {
 
 constexpr int kFusedFallback = -1;
 
-template <int ITEMS>
+template <int THREADS, int ITEMS>
 int launch_fused(const PlanArgs &a, const FusedIn &in, int grid, size_t smem, bool stats,
                  cudaStream_t s) {
-    auto fn = stats ? k_fused_small<ITEMS, true> : k_fused_small<ITEMS, false>;
+    auto fn = stats ? k_fused_small<THREADS, ITEMS, true> : k_fused_small<THREADS, ITEMS, false>;
     MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<grid, kFusedThreads, smem, s>>>(a, in);
+    fn<<<grid, THREADS, smem, s>>>(a, in);
     MP_CUDA(cudaGetLastError());
     g_launches++;
     return MP_OK;
@@ -1223,10 +1266,13 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
                int64_t *offsets_d, int64_t *peaks_d, int flags, int device, cudaStream_t s) {
     if (nmax > kFusedMaxBlocks || (flags & MP_FORCE_GLOBAL) || getenv("MEMPLAN_NO_FUSED"))
         return kFusedFallback;
-    const int items = nmax <= 256 ? 2 : (nmax <= 512 ? 4 : 16);
-    const size_t prep_smem = items == 2 ? sizeof(SmallPrep<2>::Shared)
-                            : items == 4 ? sizeof(SmallPrep<4>::Shared)
-                                         : sizeof(SmallPrep<16>::Shared);
+    // CTA shape by size: one warp (the planner's own) for tiny traces, so the
+    // register-heavy step loop does not cap residency; 256 threads for K0's
+    // block sorts beyond that
+    const int variant = nmax <= 128 ? 0 : (nmax <= 512 ? 1 : 2);
+    const size_t prep_smem = variant == 0 ? sizeof(SmallPrep<32, 8>::Shared)
+                           : variant == 1 ? sizeof(SmallPrep<128, 8>::Shared)
+                                          : sizeof(SmallPrep<256, 16>::Shared);
     // planner layout (TIER_SCAN), sized for 64-bit heights so either fits
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1243,7 +1289,8 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     const int64_t nchunks = N / 32 + T + 1;
     const size_t bytes = 2 * Carver::need<uint32_t>(32 * nchunks) + Carver::need<Rec>(N) +
                          Carver::need<uint2>(N) + Carver::need<uint32_t>(T) +
-                         4 * Carver::need<int64_t>(T) + Carver::need<int64_t>(T * ST_N);
+                         4 * Carver::need<int64_t>(T) + Carver::need<int64_t>(T * ST_N) +
+                         Carver::need<int64_t>(ST_N + 2);
     Scratch sc;
     MP_TRY(sc.alloc(bytes, s));
     Carver cv(sc.ptr, bytes);
@@ -1262,6 +1309,7 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     in.tspan = cv.take<int64_t>(T);
     in.total_units = reinterpret_cast<uint64_t *>(cv.take<int64_t>(T));
     int64_t *stats = cv.take<int64_t>(T * ST_N);
+    int64_t *red = cv.take<int64_t>(ST_N + 2);
     in.alloc = alloc_d;
     in.free_ = free_d;
     in.size = size_d;
@@ -1279,28 +1327,34 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     cudaEventCreate(&k1);
     const int64_t launches0 = g_launches;
     cudaEventRecord(k0, s);
-    int rc = items == 2 ? launch_fused<2>(a, in, (int)T, smem, stats_on, s)
-           : items == 4 ? launch_fused<4>(a, in, (int)T, smem, stats_on, s)
-                        : launch_fused<16>(a, in, (int)T, smem, stats_on, s);
-    if (rc != MP_OK) return rc;
+    int rc = variant == 0 ? launch_fused<32, 8>(a, in, (int)T, smem, stats_on, s)
+           : variant == 1 ? launch_fused<128, 8>(a, in, (int)T, smem, stats_on, s)
+                          : launch_fused<256, 16>(a, in, (int)T, smem, stats_on, s);
+    if (rc != MP_OK) {
+        cudaEventDestroy(k0);
+        cudaEventDestroy(k1);
+        return rc;
+    }
     cudaEventRecord(k1, s);
-    std::vector<int64_t> hst((size_t)T * ST_N);
-    MP_CUDA(cudaMemcpyAsync(hst.data(), stats, sizeof(int64_t) * T * ST_N,
-                            cudaMemcpyDeviceToHost, s));
+    k_reduce_stats<<<1, kRedThreads, 0, s>>>(stats, T, red);
+    MP_CUDA(cudaGetLastError());
+    g_launches++;
+    std::vector<int64_t> hst(ST_N + 2);
+    MP_CUDA(cudaMemcpyAsync(hst.data(), red, sizeof(int64_t) * (ST_N + 2), cudaMemcpyDeviceToHost,
+                            s));
     MP_CUDA(cudaStreamSynchronize(s));
-    for (int64_t t = 0; t < T; t++)
-        if (hst[t * ST_N + ST_STATUS] == PS_LINES_OVERFLOW) return kFusedFallback;
     float ms = 0;
     cudaEventElapsedTime(&ms, k0, k1);
     cudaEventDestroy(k0);
     cudaEventDestroy(k1);
+    if (hst[ST_N] > 0) return kFusedFallback;
     g_info.prep_ms = 0;
     g_info.plan_ms = ms;
     g_info.kernel_ms = ms;
     g_info.launches = g_launches - launches0;
     g_info.engine = 8 | 2 | (lay.rec_smem ? 1 : 0) | 128 | 256;  // 256: fused small-trace path
     g_info.cluster = 1;
-    return collect_stats(hst, T);
+    return collect_stats(hst, 1);
 }
 
 }  // namespace
