@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmemplan_b200.so")
+# MEMPLAN_LIB: an alternative build of the same library (A/B tuning runs)
+LIB_PATH = os.environ.get("MEMPLAN_LIB") or os.path.join(_HERE, "_lib", "libmemplan_b200.so")
 
 # status codes (include/memplan_b200.h: mp_status)
 MP_OK = 0

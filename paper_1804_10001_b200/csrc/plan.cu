@@ -1016,6 +1016,18 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
                                                                    : (int)blockIdx.x);
 }
 
+// Batched variant: capped at 168 registers so 12 single-warp CTAs (traces)
+// fit an SM's register file instead of 9; the step loop barely spills, and
+// the extra resident traces hide the step chain's fixed-latency stalls
+// (+22 % blocks/s at 12 traces per SM; a lone trace is ~13 % slower, so
+// single traces keep the uncapped kernel).
+constexpr int kOccCtas = 10;  // minBlocks hint that yields the 168-register cap
+template <typename HT, bool LINES_SMEM, bool STATS, int TIER>
+__global__ void __launch_bounds__(32, kOccCtas) k_plan_occ(PlanArgs a) {
+    plan_trace<HT, LINES_SMEM, STATS, 1, TIER, false>(a, a.tlist ? a.tlist[blockIdx.x]
+                                                                 : (int)blockIdx.x);
+}
+
 // Fused small-trace path: one CTA per trace runs K0 for its trace in shared
 // memory (prep_small), then its warp 0 runs the TIER_SCAN step loop.
 template <int THREADS, int ITEMS, bool STATS>
@@ -1081,10 +1093,14 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_stats(const int64_t *st,
 thread_local int64_t g_launches = 0;
 thread_local int g_nwarps = 1;  // warps per trace chosen by plan_device
 thread_local int g_carveout = -1;  // shared-memory carveout percent (-1: driver default)
+thread_local bool g_occ = false;   // batched launch: use the register-capped k_plan_occ
 
 template <typename HT, bool Ls, bool ST, int NW, int TIER, bool TM>
 int launch_kt(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
     auto fn = k_plan<HT, Ls, ST, NW, TIER, TM>;
+    if constexpr (sizeof(HT) == 4 && Ls && NW == 1 && !TM) {
+        if (g_occ) fn = k_plan_occ<HT, Ls, ST, TIER>;
+    }
     // always opt in: dynamic + static shared memory may pass 48 KB even when
     // the dynamic part alone does not
     MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1447,7 +1463,10 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     // highest tier that fits that budget.
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    int conc = (int)std::min<int64_t>((T + sms - 1) / sms, 8);
+    // more than one trace per SM: the register-capped kernel, up to 12 per SM
+    g_occ = T > sms;
+    if (const char *env = getenv("MEMPLAN_OCC")) g_occ = atoi(env) != 0;
+    int conc = (int)std::min<int64_t>((T + sms - 1) / sms, g_occ ? 12 : 8);
     if (const char *env = getenv("MEMPLAN_CONC")) conc = std::max(1, std::min(32, atoi(env)));
     const int lcap_s = (int)std::min<int64_t>(lneed, conc > 1 ? 256 : 1024);
     const size_t budget =
