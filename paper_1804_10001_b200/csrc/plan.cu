@@ -45,6 +45,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "common.h"
@@ -607,8 +608,13 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
 
 // The step loop for trace t, run by threads [0, 32*NW) of the CTA (k_plan
 // launches exactly those; the fused small-trace kernel hands its warp 0 in).
-template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER, bool TIMING>
+// LEAN: 32-bit step counters.  Frees the registers the capped batched kernel
+// would otherwise spill; the uncapped single-trace kernels schedule better
+// with 64-bit ones (measured, TIER_ALL 10^4: 5-7 %).
+template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER, bool TIMING,
+          bool LEAN = false>
 __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
+    using Cnt = std::conditional_t<LEAN, int, int64_t>;
     using KO = KeyT<HT>;
     using K = typename KO::K;
     using LR = LineRec<K>;
@@ -717,9 +723,9 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
     // leader-warp state (warp 0; uniform across its lanes)
     int nl = 1;
     HT peak = 0;
-    int64_t steps = 0, lifts = 0;
+    Cnt steps = 0, lifts = 0;  // < 3n + 5 < 2^31 (n < 2^26)
     int placed = 0, status = PS_OK, maxl = 1;
-    const int64_t bound = 3 * (int64_t)n + 4;
+    const Cnt bound = 3 * (Cnt)n + 4;
     // the lowest line is known without a scan after a place that leaves a
     // shoulder: the shoulder keeps the chosen (minimal) height and nothing
     // else at that height lies to its left
@@ -1024,7 +1030,7 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
 constexpr int kOccCtas = 10;  // minBlocks hint that yields the 168-register cap
 template <typename HT, bool LINES_SMEM, bool STATS, int TIER>
 __global__ void __launch_bounds__(32, kOccCtas) k_plan_occ(PlanArgs a) {
-    plan_trace<HT, LINES_SMEM, STATS, 1, TIER, false>(a, a.tlist ? a.tlist[blockIdx.x]
+    plan_trace<HT, LINES_SMEM, STATS, 1, TIER, false, true>(a, a.tlist ? a.tlist[blockIdx.x]
                                                                  : (int)blockIdx.x);
 }
 
@@ -1040,9 +1046,9 @@ __global__ void __launch_bounds__(THREADS) k_fused_small(PlanArgs a, FusedIn in)
                           const_cast<uint2 *>(a.raw2), t, smem);
     if (threadIdx.x >= 32) return;
     if (n == 0 || in.total_units[t] < (uint64_t(1) << 32))
-        plan_trace<uint32_t, true, STATS, 1, TIER_SCAN, false>(a, t);
+        plan_trace<uint32_t, true, STATS, 1, TIER_SCAN, false, true>(a, t);
     else
-        plan_trace<uint64_t, true, STATS, 1, TIER_SCAN, false>(a, t);
+        plan_trace<uint64_t, true, STATS, 1, TIER_SCAN, false, true>(a, t);
 }
 
 constexpr int64_t kFusedMaxBlocks = 2048;
