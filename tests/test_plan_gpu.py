@@ -187,3 +187,55 @@ def test_large_batch_composite_key_prep():
     for t, (a, f, s) in enumerate(cols):
         ooff, opeak = oracle.solve_bestfit(a, f, s)
         assert peaks[t] == opeak and np.array_equal(off[tp[t]:tp[t + 1]], ooff), t
+
+
+def _batch(cols):
+    tp = np.zeros(len(cols) + 1, np.int64)
+    np.cumsum([len(c[0]) for c in cols], out=tp[1:])
+    cat = [np.concatenate([c[k] for c in cols]) if tp[-1] else np.zeros(0, np.int64)
+           for k in range(3)]
+    return tp, cat
+
+
+def _check_batch(cols):
+    from paper_1804_10001_b200.bestfit import solve_bestfit_batched_arrays, plan_info
+    tp, (A, F, S) = _batch(cols)
+    off, peaks = solve_bestfit_batched_arrays(tp, A, F, S)
+    info = plan_info()
+    for t, (a, f, s) in enumerate(cols):
+        ooff, opeak = oracle.solve_bestfit(a, f, s)
+        assert peaks[t] == opeak and np.array_equal(off[tp[t]:tp[t + 1]], ooff), t
+    return info
+
+
+@pytest.mark.parametrize("lo,hi", [(0, 128), (100, 512), (400, 2048)])
+def test_fused_small_trace_path(lo, hi):
+    """Traces of <= 2048 blocks run K0 + planner in one CTA per trace (one-warp
+    CTAs up to 128 blocks, 4 / 8 warps beyond); more traces than SMs."""
+    from paper_1804_10001_b200.workloads import uniform_arrays
+    rng = np.random.default_rng(lo)
+    cols = []
+    for i in range(200 if hi <= 512 else 40):
+        n = int(rng.integers(lo, hi + 1))
+        a, f, s = uniform_arrays(n, 1000 + i) if n else (np.zeros(0, np.int64),) * 3
+        d = int(rng.integers(0, 5))
+        cols.append((a + d, f + d, ((s + 511) // 512) * 512))
+    info = _check_batch(cols)
+    assert info["engine"] & 256, info  # the fused path ran
+
+
+@pytest.mark.parametrize("tier", ["0", "1", "2", "3", "4"])
+def test_register_capped_batched_kernel(monkeypatch, tier):
+    """More traces than SMs (and traces too large for the fused path) select
+    the 168-register batched kernel and up to 12 traces per SM; every shared
+    memory tier of it must reproduce the oracle."""
+    from paper_1804_10001_b200.workloads import uniform_arrays
+    monkeypatch.setenv("MEMPLAN_TIER", tier)
+    rng = np.random.default_rng(7)
+    cols = []
+    for i in range(160):
+        n = int(rng.integers(2049, 2600))
+        a, f, s = uniform_arrays(n, 500 + i)
+        cols.append((a, f, ((s + 511) // 512) * 512))
+    info = _check_batch(cols)
+    assert not info["engine"] & 256
