@@ -61,13 +61,16 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kPendCap = 256;  // pending segment slots per warp (shared memory)
-constexpr int kG = 4;          // flagged groups evaluated per memory round
 
 // Shared-memory tiers for the window structures: nothing / group skeleton /
 // + chunk skeleton / + chunk-sorted table.
 // TIER_SCAN: small traces keep the table in shared memory and scan their
 // (short) windows row by row — no skeletons to maintain at all.
 enum { TIER_GLOBAL = 0, TIER_GROUP = 1, TIER_SKEL = 2, TIER_ALL = 3, TIER_SCAN = 4 };
+// flagged groups evaluated per memory round: 4 with the chunk skeletons in
+// shared memory (tier SKEL, single traces), else 3 — fewer live registers
+// (+3 % batched, 10^4 single traces) outweigh the memory-level parallelism
+template <int TIER> constexpr int kGroupsPerRound = TIER == TIER_SKEL ? 4 : 3;
 constexpr int64_t kScanMaxBlocks = 4096;
 
 struct PlanArgs {
@@ -463,6 +466,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
     if constexpr (TIER == TIER_SCAN)
         return query_scan<STATS, NW>(w, rec4, raw2, c0, c1, chi, clop, chip, warp, lane, lbest,
                                      r0, r1, rw, qs, rec_smem);
+    constexpr int kG = kGroupsPerRound<TIER>;
     const uint32_t thr = (chi << 5) | 31u;
     uint32_t best = kNone;
     const bool partial = (clop & 31u) != 0;
