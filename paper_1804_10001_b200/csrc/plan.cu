@@ -45,6 +45,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -1104,6 +1105,10 @@ thread_local int64_t g_launches = 0;
 thread_local int g_nwarps = 1;  // warps per trace chosen by plan_device
 thread_local int g_carveout = -1;  // shared-memory carveout percent (-1: driver default)
 thread_local bool g_occ = false;   // batched launch: use the register-capped k_plan_occ
+// Function attributes are per process: setting them and launching is one
+// critical section, so concurrent plans (pipelined halves, user threads)
+// cannot lower each other's shared-memory opt-in between set and launch.
+std::mutex g_launch_mu;
 
 template <typename HT, bool Ls, bool ST, int NW, int TIER, bool TM>
 int launch_kt(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
@@ -1113,6 +1118,7 @@ int launch_kt(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
     }
     // always opt in: dynamic + static shared memory may pass 48 KB even when
     // the dynamic part alone does not
+    std::lock_guard<std::mutex> lock(g_launch_mu);
     MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // keep only the shared memory the resident CTAs need: the rest is L1,
     // which caches the L2-resident window table between steps
@@ -1276,6 +1282,7 @@ template <int THREADS, int ITEMS>
 int launch_fused(const PlanArgs &a, const FusedIn &in, int grid, size_t smem, bool stats,
                  cudaStream_t s) {
     auto fn = stats ? k_fused_small<THREADS, ITEMS, true> : k_fused_small<THREADS, ITEMS, false>;
+    std::lock_guard<std::mutex> lock(g_launch_mu);
     MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<grid, THREADS, smem, s>>>(a, in);
     MP_CUDA(cudaGetLastError());
