@@ -10,6 +10,8 @@
 // the trace index (LSD order), so a single pass handles one or many traces.
 #include <cub/cub.cuh>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.h"
@@ -360,23 +362,27 @@ __global__ void k_group_skel(const int64_t *__restrict__ trace_ptr, int64_t T,
 }
 
 // Batch-wide key ranges for the composite-key sorts: [0] min alloc,
-// [1] max free, [2] max lifetime, [3] max size.
+// [1] max free, [2] max lifetime, [3] max size, [4] OR of all sizes (its
+// trailing zeros divide every size: dropped from the priority key).
 __global__ void k_ranges(const int64_t *__restrict__ alloc, const int64_t *__restrict__ free_,
                          const int64_t *__restrict__ size, int64_t N,
                          unsigned long long *__restrict__ out) {
     int64_t mn = INT64_MAX, mx = INT64_MIN, ml = 0, ms = 0;
+    unsigned long long so = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
          i += (int64_t)gridDim.x * blockDim.x) {
         mn = min(mn, alloc[i]);
         mx = max(mx, free_[i]);
         ml = max(ml, free_[i] - alloc[i]);
         ms = max(ms, size[i]);
+        so |= (unsigned long long)size[i];
     }
     for (int o = 16; o; o >>= 1) {
         mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
         mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
         ml = max(ml, __shfl_xor_sync(0xFFFFFFFFu, ml, o));
         ms = max(ms, __shfl_xor_sync(0xFFFFFFFFu, ms, o));
+        so |= __shfl_xor_sync(0xFFFFFFFFu, so, o);
     }
     if ((threadIdx.x & 31) == 0) {
         // order-preserving unsigned images of the signed values
@@ -384,7 +390,33 @@ __global__ void k_ranges(const int64_t *__restrict__ alloc, const int64_t *__res
         atomicMax(out + 1, (unsigned long long)mx ^ 0x8000000000000000ull);
         atomicMax(out + 2, (unsigned long long)ml);
         atomicMax(out + 3, (unsigned long long)ms);
+        atomicOr(out + 4, so);
     }
+}
+
+// Raw-time ranks: when the batch's time span fits kRankBits - 1 bits, the
+// time relative to the trace's first alloc is already an order-preserving
+// rank that fits the window keys, so the rank compression (one sort of all
+// 2N times, flags, scan, scatter) is skipped.  The best-fit loop only
+// compares times (bestfit.py:115-122, :157, :215), so any strictly
+// monotone relabelling gives the same plan.
+__global__ void k_raw_ranks(const int64_t *__restrict__ alloc, const int64_t *__restrict__ free_,
+                            const uint32_t *__restrict__ tix, const int64_t *__restrict__ tmin,
+                            int64_t N, uint32_t *__restrict__ arank, uint32_t *__restrict__ frank) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = tmin[tix[i]];
+        arank[i] = (uint32_t)(alloc[i] - m);
+        frank[i] = (uint32_t)(free_[i] - m);
+    }
+}
+
+// U = rank of the trace's last time + 1 (the sentinel line's lo is U - 1).
+__global__ void k_raw_U(const int64_t *__restrict__ trace_ptr, const int64_t *__restrict__ tspan,
+                        int64_t T, uint32_t *__restrict__ U) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T;
+         t += (int64_t)gridDim.x * blockDim.x)
+        U[t] = trace_ptr[t + 1] > trace_ptr[t] ? (uint32_t)tspan[t] + 1u : 0u;
 }
 
 // composite (trace, time - tmin) keys over alloc ∪ free; idx = iota
@@ -414,12 +446,14 @@ __global__ void k_arank_keys(const uint32_t *__restrict__ arank, const uint32_t 
 // composite (trace, lifetime desc, size desc) keys; ids ascend by stability
 __global__ void k_prio_keys(const int64_t *__restrict__ alloc, const int64_t *__restrict__ free_,
                             const int64_t *__restrict__ size, const uint32_t *__restrict__ tix,
-                            int64_t N, int lbits, int sbits, uint64_t lmax, uint64_t smax,
-                            uint64_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+                            int64_t N, int lbits, int sbits, int sshift, uint64_t lmax,
+                            uint64_t smax, uint64_t *__restrict__ keys,
+                            uint32_t *__restrict__ vals) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t life = (uint64_t)(free_[i] - alloc[i]), sz = (uint64_t)size[i];
-        keys[i] = ((uint64_t)tix[i] << (lbits + sbits)) | ((lmax - life) << sbits) | (smax - sz);
+        keys[i] = ((uint64_t)tix[i] << (lbits + sbits)) | ((lmax - life) << sbits) |
+                  ((smax - sz) >> sshift);
         vals[i] = (uint32_t)i;
     }
 }
@@ -516,17 +550,17 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
     // Large batches: one composite-key sort per ordering instead of a full
     // 64-bit sort plus a stable regroup by trace, with the key widths cut to
     // the batch's actual ranges (one small reduction + one host sync).
-    bool comp = false;
-    int tbits = 0, lbits = 0, sbits = 0;
+    bool comp = false, raw = false;
+    int tbits = 0, lbits = 0, sbits = 0, sshift = 0;
     uint64_t lmax = 0, smax = 0;
     int64_t tmin = 0;
     if (T > 1 && N >= (int64_t(1) << 16)) {
         unsigned long long *rng = reinterpret_cast<unsigned long long *>(k64_s);
-        const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+        const unsigned long long init[5] = {~0ull, 0ull, 0ull, 0ull, 0ull};
         MP_CUDA(cudaMemcpyAsync(rng, init, sizeof(init), cudaMemcpyHostToDevice, s));
         k_ranges<<<std::min(g1, 148 * 8), kThreads, 0, s>>>(in.alloc, in.free_, in.size, N, rng);
         g_prep_k++;
-        unsigned long long h[4];
+        unsigned long long h[5];
         MP_CUDA(cudaMemcpyAsync(h, rng, sizeof(h), cudaMemcpyDeviceToHost, s));
         MP_CUDA(cudaStreamSynchronize(s));
         tmin = (int64_t)(h[0] ^ 0x8000000000000000ull);
@@ -535,13 +569,25 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
         tbits = bits_for_u64(span);
         lmax = h[2];
         smax = h[3];
+        sshift = h[4] ? __builtin_ctzll(h[4]) : 0;
         lbits = bits_for_u64(lmax);
-        sbits = bits_for_u64(smax);
+        sbits = bits_for_u64(smax >> sshift);
         comp = tb + tbits <= 64 && tb + lbits + sbits <= 64 && tmax >= tmin;
+        raw = comp && tbits < kRankBits - 1 && !getenv("MEMPLAN_DENSE_RANKS");
     }
     // ---- compressed time ranks over alloc ∪ free, per trace ----
     size_t tb_ = tbytes;
     uint32_t *rk_idx = idx_s;
+    if (raw) {
+        k_trace_scale<<<(unsigned)T, kThreads, 0, s>>>(in.trace_ptr, in.size, in.alloc, in.free_,
+                                                      out.unit, out.total_units, out.tmin,
+                                                      out.tspan);
+        g_prep_k++;
+        k_raw_ranks<<<g1, kThreads, 0, s>>>(in.alloc, in.free_, tix, out.tmin, N, arank, frank);
+        g_prep_k++;
+        k_raw_U<<<grid_for(T), kThreads, 0, s>>>(in.trace_ptr, out.tspan, T, out.U);
+        g_prep_k++;
+    } else {
     if (comp) {
         uint64_t *tk64 = reinterpret_cast<uint64_t *>(times), *tk64_s = reinterpret_cast<uint64_t *>(times_s);
         k_time_keys<<<g2, kThreads, 0, s>>>(in.alloc, in.free_, tix, N, tmin, tbits, tk64, idx);
@@ -570,10 +616,12 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
     g_prep_k++;
     k_trace_U<<<grid_for(T), kThreads, 0, s>>>(scan, in.trace_ptr, T, out.U);
     g_prep_k++;
+    }
 
     // ---- (alloc, id) order: stable by alloc rank, then stable by trace ----
     uint32_t *ka = tk, *ka_s = tk_s, *va = idx, *va_s = idx_s;
-    const int rbits = bits_for_u64((uint64_t)(2 * N + 2));  // ranks < 2n+1 per trace
+    // ranks < 2n+1 per trace (dense) or <= the batch's time span (raw)
+    const int rbits = raw ? std::max(1, tbits) : bits_for_u64((uint64_t)(2 * N + 2));
     const bool comp32 = comp && tb + rbits <= 32;
     if (comp32) {
         k_arank_keys<<<g1, kThreads, 0, s>>>(arank, tix, N, rbits, ka, va);
@@ -605,8 +653,8 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
     uint32_t *vp = idx, *vp_s = idx_s;
     uint32_t *pord = nullptr;
     if (comp) {
-        k_prio_keys<<<g1, kThreads, 0, s>>>(in.alloc, in.free_, in.size, tix, N, lbits, sbits, lmax,
-                                            smax, k64, vp);
+        k_prio_keys<<<g1, kThreads, 0, s>>>(in.alloc, in.free_, in.size, tix, N, lbits, sbits,
+                                            sshift, lmax, smax, k64, vp);
         g_prep_k++;
         tb_ = tbytes;
         MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_, k64, k64_s, vp, vp_s, (int)N, 0,
@@ -633,10 +681,12 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
     k_inverse<<<g1, kThreads, 0, s>>>(pord, tix, in.trace_ptr, N, prio);
     g_prep_k++;
 
-    k_trace_scale<<<(unsigned)T, kThreads, 0, s>>>(in.trace_ptr, in.size, in.alloc, in.free_,
-                                                  out.unit, out.total_units, out.tmin,
-                                                  out.tspan);
-    g_prep_k++;
+    if (!raw) {
+        k_trace_scale<<<(unsigned)T, kThreads, 0, s>>>(in.trace_ptr, in.size, in.alloc, in.free_,
+                                                      out.unit, out.total_units, out.tmin,
+                                                      out.tspan);
+        g_prep_k++;
+    }
     k_pack<<<g1, kThreads, 0, s>>>(tix, in.trace_ptr, arank, frank, posof, prio, sar, in.size,
                                    out.unit, in.alloc, in.free_, out.tmin, N, out.ent, out.rec,
                                    out.raw2, out.rawpos);

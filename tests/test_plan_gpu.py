@@ -163,13 +163,22 @@ def test_every_layout_tier_and_warp_count(monkeypatch, nwarps, tier):
         assert peaks[t] == opeak and np.array_equal(off[sl], ooff)
 
 
-def test_large_batch_composite_key_prep():
+@pytest.mark.parametrize("mode", ["raw", "dense", "wide"])
+def test_large_batch_composite_key_prep(monkeypatch, mode):
     """Batches of >= 2^16 blocks take K0's composite-key sorts (one sort per
-    ordering, key widths cut to the batch's ranges); every trace must match."""
+    ordering, key widths cut to the batch's ranges); with a time span below
+    2^25 the raw relative times serve as ranks (no rank compression),
+    otherwise (MEMPLAN_DENSE_RANKS, or a wide span) ranks are compressed.
+    Every trace must match the oracle in every mode."""
     from paper_1804_10001_b200.bestfit import solve_bestfit_batched_arrays
     from paper_1804_10001_b200.workloads import uniform_arrays
     import paper_1804_10001_b200 as mp
+    if mode == "dense":
+        monkeypatch.setenv("MEMPLAN_DENSE_RANKS", "1")
     cols = []
+    if mode == "wide":  # a far-away trace: batch span >= 2^25
+        a, f, s = uniform_arrays(3000, 77)
+        cols.append((a + (1 << 40), f + (1 << 40), ((s + 511) // 512) * 512))
     for i in range(6):
         a, f, s = uniform_arrays(10000 + 37 * i, 300 + i)
         cols.append((a + 1000 * i, f + 1000 * i, ((s + 511) // 512) * 512))
