@@ -164,9 +164,10 @@ struct Win {
     uint64_t keep, stream;  // L2 policies (global tiers)
 };
 
-// L2 cache policies for the global-memory tiers: the skeletons are the hot,
-// re-read working set of every step (evict_last); records are read once per
-// placement (evict_first).
+// L2 cache policies for the global-memory tiers: the group / S0 skeletons are
+// the hot, re-read working set of every step (evict_last); everything else
+// is evict_normal — evict_first on S1/S2, records and raw times cost 3 % at
+// 12 traces per SM (those lines are re-read by later steps of the same trace).
 __device__ __forceinline__ uint64_t l2_policy_keep() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -174,7 +175,7 @@ __device__ __forceinline__ uint64_t l2_policy_keep() {
 }
 __device__ __forceinline__ uint64_t l2_policy_stream() {
     uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ uint4 ldg_hint(const uint4 *ptr, uint64_t pol) {
