@@ -2,7 +2,7 @@
 
 Workload (BASELINE.json configs[4], "synthetic random-lifetime traces, 10^4-
 10^6 blocks ... vs host-CPU reference"): every GPU plans a batch of
---traces (default 1776 = 12 per SM) synthetic uniform-random-lifetime traces
+--traces (default 2368 = 16 per SM) synthetic uniform-random-lifetime traces
 of --n (default 10^5) blocks each
 (alloc ~ U[0,2n), free ~ U(alloc, 2n], size ~ U[1, 2^20] rounded to 512 B),
 seeded per rank -> weak scaling.  One step = one batched plan of the
@@ -494,7 +494,7 @@ def main():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--blocks", dest="n", type=int, default=100_000,
                    help="blocks per trace (not --n: torchrun would take it as its own flag)")
-    p.add_argument("--traces", type=int, default=1776)
+    p.add_argument("--traces", type=int, default=2368)
     p.add_argument("--cpu-procs", type=int, default=32)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-replay", action="store_true")

@@ -68,10 +68,15 @@ constexpr int kPendCap = 256;  // pending segment slots per warp (shared memory)
 // TIER_SCAN: small traces keep the table in shared memory and scan their
 // (short) windows row by row — no skeletons to maintain at all.
 enum { TIER_GLOBAL = 0, TIER_GROUP = 1, TIER_SKEL = 2, TIER_ALL = 3, TIER_SCAN = 4 };
-// flagged groups evaluated per memory round: 4 with the chunk skeletons in
-// shared memory (tier SKEL, single traces), else 3 — fewer live registers
-// (+3 % batched, 10^4 single traces) outweigh the memory-level parallelism
-template <int TIER> constexpr int kGroupsPerRound = TIER == TIER_SKEL ? 4 : 3;
+// Flagged groups evaluated per memory round, and pending segments read per
+// lane per wave.  Single traces: 4 groups with the chunk skeletons in shared
+// memory (tier SKEL), else 3, and 2 segments.  LEAN (the batched kernel
+// capped at 128 registers): 2 groups, 1 segment — the smallest memory-level
+// parallelism that compiles without spills at 128 registers, which is what
+// lets 16 traces share an SM (4 warps per SM sub-partition).
+template <int TIER, bool LEAN>
+constexpr int kGroupsPerRound = LEAN ? 2 : (TIER == TIER_SKEL ? 4 : 3);
+template <bool LEAN> constexpr int kSegsPerLane = LEAN ? 1 : 2;
 constexpr int64_t kScanMaxBlocks = 4096;
 
 struct PlanArgs {
@@ -274,19 +279,20 @@ __device__ __forceinline__ uint32_t fit_min4(uint4 k, uint4 v, uint32_t thr, uin
     return best;
 }
 
-// Read the pending segments — one per lane, two per lane in flight (64 per
-// wave), each as two 16-byte loads of SF and two of SP — skipping segments
-// whose prefix minimum cannot beat `bound`, which tightens after every wave.
-// Returns this lane's best fitting priority.
+// Read the pending segments — DU per lane in flight (32 * DU per wave), each
+// as two 16-byte loads of SF and two of SP — skipping segments whose prefix
+// minimum cannot beat `bound`, which tightens after every wave.  Returns
+// this lane's best fitting priority.
+template <int DU>
 __device__ __forceinline__ uint32_t drain_pending(const Win &w, const uint32_t *pend, int np,
                                                   uint32_t thr, uint32_t bound, int lane) {
     __syncwarp();
     uint32_t best = kNone;
-    for (int e0 = 0; e0 < np; e0 += 64) {
-        uint4 k[2][2], v[2][2];
-        bool act[2];
+    for (int e0 = 0; e0 < np; e0 += 32 * DU) {
+        uint4 k[DU][2], v[DU][2];
+        bool act[DU];
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
+        for (int u = 0; u < DU; u++) {
             const int e = e0 + 32 * u + lane;
             act[u] = e < np && pend[kPendCap + e] < bound;
             if (act[u]) {
@@ -301,13 +307,13 @@ __device__ __forceinline__ uint32_t drain_pending(const Win &w, const uint32_t *
             }
         }
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
+        for (int u = 0; u < DU; u++) {
             if (act[u]) {
                 best = fit_min4(k[u][0], v[u][0], thr, best);
                 best = fit_min4(k[u][1], v[u][1], thr, best);
             }
         }
-        if (e0 + 64 < np) bound = min(bound, __reduce_min_sync(kFull, best));
+        if (e0 + 32 * DU < np) bound = min(bound, __reduce_min_sync(kFull, best));
     }
     __syncwarp();
     return best;
@@ -458,7 +464,7 @@ __device__ __forceinline__ uint32_t query_scan(const Win &w, const uint4 *rec4, 
     return wb;
 }
 
-template <bool STATS, int NW, int TIER>
+template <bool STATS, int NW, int TIER, bool LEAN>
 __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4, const uint2 *raw2,
                                                  uint32_t *pend, int c0, int c1, uint32_t chi,
                                                  uint32_t clop, uint32_t chip, uint32_t rawhi,
@@ -468,7 +474,8 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
     if constexpr (TIER == TIER_SCAN)
         return query_scan<STATS, NW>(w, rec4, raw2, c0, c1, chi, clop, chip, warp, lane, lbest,
                                      r0, r1, rw, qs, rec_smem);
-    constexpr int kG = kGroupsPerRound<TIER>;
+    constexpr int kG = kGroupsPerRound<TIER, LEAN>;
+    constexpr int DU = kSegsPerLane<LEAN>;
     const uint32_t thr = (chi << 5) | 31u;
     uint32_t best = kNone;
     const bool partial = (clop & 31u) != 0;
@@ -517,7 +524,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
                                             pend, np, lane);
             if (np > kPendCap - 32 * kG) {
                 if (STATS) qs.seg += np;
-                best = min(best, drain_pending(w, pend, np, thr, kNone, lane));
+                best = min(best, drain_pending<DU>(w, pend, np, thr, kNone, lane));
                 np = 0;
             }
         }
@@ -581,7 +588,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
             }
             if (np > kPendCap - 32 * kG) {
                 if (STATS) qs.seg += np;
-                best = min(best, drain_pending(w, pend, np, thr, kNone, lane));
+                best = min(best, drain_pending<DU>(w, pend, np, thr, kNone, lane));
                 np = 0;
             }
             if (prune && __popc(m) >= 4) tighten();
@@ -602,7 +609,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
         for (int e = lane; e < np; e += 32)
             qs.seg += __popc(__ballot_sync(__activemask(), pend[kPendCap + e] < wb1));
     }
-    const uint32_t b2 = drain_pending(w, pend, np, thr, wb1, lane);
+    const uint32_t b2 = drain_pending<DU>(w, pend, np, thr, wb1, lane);
     if (b2 < best) best = b2;
     const uint32_t wb = __reduce_min_sync(kFull, best);
     if (!rec_smem && wb != wb1 && best == wb) {  // a pending segment improved it
@@ -823,7 +830,7 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
         uint2 rw = make_uint2(0, 0);
         if (qlop < qhip) {
             const int c0 = (int)(qlop >> 5), c1 = (int)((qhip - 1) >> 5);
-            wb = query_window<STATS, NW, TIER>(win, rec4, raw2, pend, c0, c1, qchi, qlop,
+            wb = query_window<STATS, NW, TIER, LEAN>(win, rec4, raw2, pend, c0, c1, qchi, qlop,
                                                qhip, qraw, prune, warp, lane, lbest, r0, r1, rw,
                                                qs, a.rec_smem != 0);
         }
@@ -1028,12 +1035,13 @@ __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
                                                                    : (int)blockIdx.x);
 }
 
-// Batched variant: capped at 168 registers so 12 single-warp CTAs (traces)
-// fit an SM's register file instead of 9; the step loop barely spills, and
-// the extra resident traces hide the step chain's fixed-latency stalls
-// (+22 % blocks/s at 12 traces per SM; a lone trace is ~13 % slower, so
-// single traces keep the uncapped kernel).
-constexpr int kOccCtas = 10;  // minBlocks hint that yields the 168-register cap
+// Batched variant: capped at 128 registers (LEAN step loop, no spills) so
+// 16 single-warp CTAs (traces) fit an SM — 4 warps per sub-partition's
+// 16 K registers — instead of 9 for the uncapped kernel; the extra resident
+// traces hide the step chain's latency (blocks/s: 9 -> 199 M, 12 at 168
+// registers -> 285 M, 16 at 128 -> 307 M).  A lone trace is slower under the
+// cap, so single traces keep the uncapped kernel.
+constexpr int kOccCtas = 16;  // minBlocks hint that yields the 128-register cap
 template <typename HT, bool LINES_SMEM, bool STATS, int TIER>
 __global__ void __launch_bounds__(32, kOccCtas) k_plan_occ(PlanArgs a) {
     plan_trace<HT, LINES_SMEM, STATS, 1, TIER, false, true>(a, a.tlist ? a.tlist[blockIdx.x]
@@ -1481,10 +1489,10 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     // highest tier that fits that budget.
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    // more than one trace per SM: the register-capped kernel, up to 12 per SM
+    // more than one trace per SM: the register-capped kernel, up to 16 per SM
     g_occ = T > sms;
     if (const char *env = getenv("MEMPLAN_OCC")) g_occ = atoi(env) != 0;
-    int conc = (int)std::min<int64_t>((T + sms - 1) / sms, g_occ ? 12 : 8);
+    int conc = (int)std::min<int64_t>((T + sms - 1) / sms, g_occ ? kOccCtas : 8);
     if (const char *env = getenv("MEMPLAN_CONC")) conc = std::max(1, std::min(32, atoi(env)));
     const int lcap_s = (int)std::min<int64_t>(lneed, conc > 1 ? 256 : 1024);
     const size_t budget =

@@ -236,7 +236,7 @@ def test_fused_small_trace_path(lo, hi):
 @pytest.mark.parametrize("tier", ["0", "1", "2", "3", "4"])
 def test_register_capped_batched_kernel(monkeypatch, tier):
     """More traces than SMs (and traces too large for the fused path) select
-    the 168-register batched kernel and up to 12 traces per SM; every shared
+    the 128-register batched kernel and up to 16 traces per SM; every shared
     memory tier of it must reproduce the oracle."""
     from paper_1804_10001_b200.workloads import uniform_arrays
     monkeypatch.setenv("MEMPLAN_TIER", tier)

@@ -2,7 +2,7 @@
 #   VARIANTS="mb1 mb16" TRACES="1184 2368" bash tools/gpu_variants.sh
 cd $GRAFT_REPO_ROOT
 for V in ${VARIANTS:-mb1}; do
-  for T in ${TRACES:-1776}; do
+  for T in ${TRACES:-2368}; do
     C=$(( (T + 147) / 148 ))
     echo "== $V T=$T conc=$C"
     MEMPLAN_LIB=tools/_variants/$V/libmemplan_b200.so MEMPLAN_CONC=$C timeout 900 \
