@@ -10,6 +10,22 @@ using namespace mp;
 
 namespace {
 
+// Pinned host staging for small host-array plans, one per thread and
+// device, allocated on first use and kept (the per-network use case plans
+// the same few-thousand-block traces over and over).
+constexpr size_t kStageBytes = size_t(4) << 20;
+
+int64_t *pinned_stage(int device) {
+    static thread_local void *stage[64] = {nullptr};
+    if (device < 0 || device >= 64) return nullptr;
+    if (!stage[device] && cudaHostAlloc(&stage[device], kStageBytes, cudaHostAllocDefault) !=
+                              cudaSuccess) {
+        cudaGetLastError();
+        stage[device] = nullptr;
+    }
+    return static_cast<int64_t *>(stage[device]);
+}
+
 int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *alloc,
                const int64_t *free_, const int64_t *size, int64_t T, int64_t *offsets_out,
                int64_t *peaks_out, int flags, int device, cudaStream_t s) {
@@ -45,20 +61,47 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
         return plan_device(tp_d, tp_h.data(), T, alloc, free_, size, offsets_out, peaks_out,
                            flags, device, s);
     }
-    // host pointers: stage through one device buffer
+    // host pointers: stage through one device buffer laid out as
+    // [trace_ptr | alloc | free | size] [offsets | peaks] so that each
+    // direction is one copy
     const size_t nb = sizeof(int64_t) * (size_t)N;
+    const size_t in_b = sizeof(int64_t) * (size_t)(T + 1) + 3 * nb;
+    const size_t out_b = nb + sizeof(int64_t) * (size_t)T;
     Scratch buf;
-    MP_TRY(buf.alloc(4 * nb + sizeof(int64_t) * (2 * T + 1) + 5 * 256, s));
-    Carver cv(buf.ptr, buf.bytes);
-    int64_t *a_d = cv.take<int64_t>(N), *f_d = cv.take<int64_t>(N), *s_d = cv.take<int64_t>(N);
-    int64_t *o_d = cv.take<int64_t>(N), *p_d = cv.take<int64_t>(T), *tp_d = cv.take<int64_t>(T + 1);
-    MP_CUDA(cudaMemcpyAsync(tp_d, tp_h.data(), sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, s));
-    if (N) {
-        MP_CUDA(cudaMemcpyAsync(a_d, alloc, nb, cudaMemcpyHostToDevice, s));
-        MP_CUDA(cudaMemcpyAsync(f_d, free_, nb, cudaMemcpyHostToDevice, s));
-        MP_CUDA(cudaMemcpyAsync(s_d, size, nb, cudaMemcpyHostToDevice, s));
+    MP_TRY(buf.alloc(in_b + out_b + 256, s));
+    int64_t *tp_d = buf.as<int64_t>();
+    int64_t *a_d = tp_d + (T + 1), *f_d = a_d + N, *s_d = f_d + N;
+    int64_t *o_d = s_d + N, *p_d = o_d + N;
+    // small plans (per-network planning) go through a pinned staging buffer:
+    // two copies instead of six pageable ones
+    int64_t *stage = (in_b <= kStageBytes && out_b <= kStageBytes) ? pinned_stage(device) : nullptr;
+    if (stage) {
+        memcpy(stage, tp_h.data(), sizeof(int64_t) * (T + 1));
+        if (N) {
+            memcpy(stage + (T + 1), alloc, nb);
+            memcpy(stage + (T + 1) + N, free_, nb);
+            memcpy(stage + (T + 1) + 2 * N, size, nb);
+        }
+        MP_CUDA(cudaMemcpyAsync(tp_d, stage, in_b, cudaMemcpyHostToDevice, s));
+    } else {
+        MP_CUDA(cudaMemcpyAsync(tp_d, tp_h.data(), sizeof(int64_t) * (T + 1),
+                                cudaMemcpyHostToDevice, s));
+        if (N) {
+            MP_CUDA(cudaMemcpyAsync(a_d, alloc, nb, cudaMemcpyHostToDevice, s));
+            MP_CUDA(cudaMemcpyAsync(f_d, free_, nb, cudaMemcpyHostToDevice, s));
+            MP_CUDA(cudaMemcpyAsync(s_d, size, nb, cudaMemcpyHostToDevice, s));
+        }
     }
     MP_TRY(plan_device(tp_d, tp_h.data(), T, a_d, f_d, s_d, o_d, p_d, flags, device, s));
+    if (stage) {
+        // the staging buffer's input part was consumed by the upload above
+        // (plan_device synchronised the stream)
+        MP_CUDA(cudaMemcpyAsync(stage, o_d, out_b, cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        if (N) memcpy(offsets_out, stage, nb);
+        if (T) memcpy(peaks_out, stage + N, sizeof(int64_t) * T);
+        return MP_OK;
+    }
     if (N) MP_CUDA(cudaMemcpyAsync(offsets_out, o_d, nb, cudaMemcpyDeviceToHost, s));
     if (T) MP_CUDA(cudaMemcpyAsync(peaks_out, p_d, sizeof(int64_t) * T, cudaMemcpyDeviceToHost, s));
     MP_CUDA(cudaStreamSynchronize(s));
