@@ -2,6 +2,7 @@
 the hot path, run through this package on the GPU."""
 import random
 
+import numpy as np
 import pytest
 
 import oracle
@@ -96,3 +97,40 @@ def test_lstm_batched_bit_exact():
         a, f, s = inst.arrays()
         off, peak = oracle.solve_bestfit(a, f, s)
         assert plan.peak == peak and list(plan.offsets.values()) == off.tolist()
+
+
+def test_full_size_properties():
+    """BASELINE's largest synthetic size (10^6 blocks), checked through
+    size-independent properties instead of the oracle: the GPU validator
+    finds no overlap and recomputes the same peak, and the clique lower
+    bound does not exceed it.  At 10^5 blocks: scaling all sizes by c scales
+    offsets and peak by c; a strictly increasing relabelling of the times
+    (shift, stretch — the stretched one leaves the raw-rank range of K0)
+    leaves every offset unchanged; the batched path equals the single one."""
+    from paper_1804_10001_b200.bestfit import solve_bestfit_arrays, solve_bestfit_batched_arrays
+    from paper_1804_10001_b200.verifier import verify_arrays, clique_lower_bound_arrays
+    from paper_1804_10001_b200.workloads import uniform_arrays
+    a, f, s = uniform_arrays(1_000_000, 11)
+    s = ((s + 511) // 512) * 512
+    off, peak = solve_bestfit_arrays(a, f, s)
+    rep = verify_arrays(a, f, s, off, viol_cap=16)
+    assert rep["n_violations"] == 0 and rep["offsets_ok"] and rep["peak_recomputed"] == peak
+    assert clique_lower_bound_arrays(a, f, s) <= peak
+    assert np.all(off % 512 == 0)
+
+    a, f, s = uniform_arrays(100_000, 12)
+    s = ((s + 511) // 512) * 512
+    off, peak = solve_bestfit_arrays(a, f, s)
+    off3, peak3 = solve_bestfit_arrays(a, f, 3 * s)
+    assert peak3 == 3 * peak and np.array_equal(off3, 3 * off)
+    for aa, ff in ((a + 12345, f + 12345), (7 * a + 3, 7 * f + 3), (1000 * a, 1000 * f)):
+        o2, p2 = solve_bestfit_arrays(aa, ff, s)
+        assert p2 == peak and np.array_equal(o2, off)
+    # three copies in one batch, one of them stretched (batch span > 2^25:
+    # dense ranks), all equal to the single plan
+    tp = np.arange(4, dtype=np.int64) * len(a)
+    A = np.concatenate([a, 1000 * a, a]); F = np.concatenate([f, 1000 * f, f])
+    offb, peaks = solve_bestfit_batched_arrays(tp, A, F, np.concatenate([s, s, s]))
+    assert list(peaks) == [peak] * 3
+    for t in range(3):
+        assert np.array_equal(offb[tp[t]:tp[t + 1]], off)
