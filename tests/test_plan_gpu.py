@@ -248,3 +248,42 @@ def test_register_capped_batched_kernel(monkeypatch, tier):
         cols.append((a, f, ((s + 511) // 512) * 512))
     info = _check_batch(cols)
     assert not info["engine"] & 256
+
+
+def test_concurrent_host_threads():
+    """Plans issued from several host threads at once (ctypes drops the GIL)
+    equal the same plans issued one after another: per-thread state and
+    the serialised attribute-set + launch keep them independent."""
+    import threading
+    from paper_1804_10001_b200.bestfit import solve_bestfit_batched_arrays, solve_bestfit_arrays
+    from paper_1804_10001_b200.workloads import uniform_arrays
+    jobs = []
+    for i in range(6):
+        cols = []
+        for k in range(3 + 60 * (i % 2)):
+            n = [40, 700, 3000, 9000][(i + k) % 4]
+            a, f, s = uniform_arrays(n, 50 * i + k)
+            cols.append((a, f, ((s + 511) // 512) * 512))
+        jobs.append(_batch(cols))
+    single = [uniform_arrays(20000, 999)]
+    ref = [solve_bestfit_batched_arrays(tp, *cat) for tp, cat in jobs]
+    ref_single = solve_bestfit_arrays(*single[0])
+    out = [None] * len(jobs)
+    out_single = [None]
+
+    def run(i):
+        tp, cat = jobs[i]
+        out[i] = solve_bestfit_batched_arrays(tp, *cat)
+
+    def run_single():
+        out_single[0] = solve_bestfit_arrays(*single[0])
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(jobs))]
+    threads.append(threading.Thread(target=run_single))
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    for (o, p), (ro, rp) in zip(out, ref):
+        assert np.array_equal(o, ro) and np.array_equal(p, rp)
+    assert np.array_equal(out_single[0][0], ref_single[0]) and out_single[0][1] == ref_single[1]
