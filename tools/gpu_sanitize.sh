@@ -19,6 +19,18 @@ inst = mp.profile_to_instance(mp.record(mp.parse_trace(mp.cnn_like_trace(mp.GenS
 solve_bestfit_arrays(*inst.arrays())
 tp = np.array([0, 1000, 1500, 3000]); solve_bestfit_batched_arrays(tp, a, f, s)
 k = np.arange(1200, dtype=np.int64); solve_bestfit_arrays(2 * k, 2 * k + 1, k + 1)
+def batch(sizes, seed):
+    cols = [uniform_arrays(n, seed + i) for i, n in enumerate(sizes)]
+    cols = [(x, y, ((z + 511) // 512) * 512) for x, y, z in cols]
+    tp = np.zeros(len(cols) + 1, np.int64); np.cumsum([len(c[0]) for c in cols], out=tp[1:])
+    return tp, [np.concatenate([c[j] for c in cols]) for j in range(3)]
+# fused path: one-warp (<= 128 blocks) and 4-warp CTAs, more traces than SMs
+for sizes in ([13] * 300, [400] * 200):
+    tp, cat = batch(sizes, 7)
+    solve_bestfit_batched_arrays(tp, *cat)
+# register-capped LEAN batched kernel + composite / raw-rank K0 (N >= 2^16)
+tp, cat = batch([2100] * 160, 11)
+solve_bestfit_batched_arrays(tp, *cat)
 print("case ok", pk)
 PY
 for tool in memcheck racecheck synccheck; do
