@@ -182,6 +182,10 @@ typedef struct {
     int64_t pool_last_ref;  /* fallback.last_ref         */
 } mp_arena_state;
 
+/* The arena's fallback pool (Arena.fallback, arena.py:172), owned by the
+ * arena: usable with every mp_pool_* call, never mp_pool_destroy'd. */
+struct mp_pool;
+struct mp_pool *mp_arena_pool(mp_arena *a);
 int mp_arena_get_state(mp_arena *a, mp_arena_state *out);
 /* Current plan tables (n_blocks entries each; any pointer may be NULL). */
 int mp_arena_get_plan(mp_arena *a, int64_t *offsets, int64_t *sizes,
@@ -229,6 +233,21 @@ int mp_torch_replay_end(void);
  * epoch once a free happens off its planned tick, so a run that deviates
  * from the profile can never alias live memory. */
 int mp_torch_stats(int64_t *n_planned, int64_t *n_side, int64_t *n_diverged);
+/* Extended replay counters (same clock as mp_torch_stats) plus the region
+ * state: deferred re-plans done at epoch boundaries (Arena.reoptimize,
+ * arena.py:303-322, run on the GPU planner when an epoch saw growth),
+ * planned blocks carried live across an epoch boundary (their range stays
+ * reserved; an overlapping planned request of the next epoch is served from
+ * a side allocation), regions still held (the current one plus retired ones
+ * with carried blocks), frees of unknown pointers inside a region (never
+ * passed to cudaFree), live side allocations. */
+typedef struct {
+    int64_t n_planned, n_side, n_diverged, n_replans;
+    int64_t n_carried_live, n_regions, n_unknown_free, n_side_live;
+    uint64_t region_base;
+    int64_t region_bytes, plan_peak;
+} mp_torch_stats_t;
+int mp_torch_stats_ex(mp_torch_stats_t *out);
 /* Benchmark helper: replay the epoch `reps` times through mp_torch_alloc /
  * mp_torch_free directly (replay mode), best mean host ns per alloc call. */
 int mp_torch_bench(const int32_t *kinds, const int64_t *values, int64_t n_events, int64_t reps,

@@ -67,6 +67,15 @@ class ArenaState(ctypes.Structure):
         "n_live", "depth", "plan_version", "pool_last_ref")]
 
 
+class TorchStats(ctypes.Structure):
+    """mp_torch_stats_t (include/memplan_b200.h)."""
+    _fields_ = [(k, ctypes.c_int64) for k in
+                ("n_planned", "n_side", "n_diverged", "n_replans", "n_carried_live",
+                 "n_regions", "n_unknown_free", "n_side_live")] + \
+               [("region_base", ctypes.c_uint64), ("region_bytes", ctypes.c_int64),
+                ("plan_peak", ctypes.c_int64)]
+
+
 class IngestInfo(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
         "n_blocks", "unmanaged_count", "horizon", "n_events", "err_line", "err_tok_off",
@@ -101,6 +110,7 @@ SIGNATURES = [
     ("mp_arena_resume", ctypes.c_int, [VP]),
     ("mp_arena_close", ctypes.c_int, [VP]),
     ("mp_arena_reoptimize", ctypes.c_int, [VP]),
+    ("mp_arena_pool", VP, [VP]),
     ("mp_arena_get_state", ctypes.c_int, [VP, ctypes.POINTER(ArenaState)]),
     ("mp_arena_get_plan", ctypes.c_int, [VP, VP, VP, VP, VP]),
     ("mp_arena_get_live", ctypes.c_int, [VP, VP, VP, VP]),
@@ -116,6 +126,7 @@ SIGNATURES = [
     ("mp_torch_replay_begin", ctypes.c_int, [VP, ctypes.c_int, PU64]),
     ("mp_torch_replay_end", ctypes.c_int, []),
     ("mp_torch_stats", ctypes.c_int, [P64, P64, P64]),
+    ("mp_torch_stats_ex", ctypes.c_int, [ctypes.POINTER(TorchStats)]),
     ("mp_torch_bench", ctypes.c_int, [VP, VP, ctypes.c_int64, ctypes.c_int64,
                                       ctypes.POINTER(ctypes.c_double)]),
     ("mp_pool_create", ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(VP)]),

@@ -71,12 +71,22 @@ class PoolAllocator:
         h = N.VP()
         _check(N.lib().mp_pool_create(-1 if capacity is None else capacity, ctypes.byref(h)))
         self._h = h
+        self._owner = None
+
+    @classmethod
+    def _borrow(cls, handle, owner) -> "PoolAllocator":
+        """View of a pool owned by someone else (the arena's fallback)."""
+        p = cls.__new__(cls)
+        p.capacity = None
+        p._h = N.VP(handle)
+        p._owner = owner  # keeps the owning arena alive; never destroyed here
+        return p
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and getattr(self, "_owner", None) is None:
             N.lib().mp_pool_destroy(h)
-            self._h = None
+        self._h = None
 
     def _stats(self):
         vals = [ctypes.c_int64() for _ in range(4)]
@@ -105,21 +115,6 @@ class PoolAllocator:
 
     def live_bytes(self) -> int:
         return self._stats()[2]
-
-
-class _PoolView:
-    """Read-only view of an arena's fallback pool (Arena.fallback)."""
-
-    def __init__(self, arena: "Arena"):
-        self._arena = arena
-
-    @property
-    def peak(self) -> int:
-        return self._arena._state().pool_peak
-
-    @property
-    def last_ref(self) -> int:
-        return self._arena._state().pool_last_ref
 
 
 class Arena:
@@ -152,7 +147,8 @@ class Arena:
         self._h = h
         self._plan = plan
         self._plan_version = 0
-        self.fallback = _PoolView(self)
+        # the arena's own pool (reference: a PoolAllocator, arena.py:172)
+        self.fallback = PoolAllocator._borrow(N.lib().mp_arena_pool(h), self)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -259,9 +255,15 @@ class Arena:
 
 def replay_events(arena: Arena, events) -> list:
     """Drive one epoch's events through the arena; addresses served to the
-    allocations in order.  Does not reset (reference arena.py:325-340)."""
-    kinds, values = encode_events(events)
-    return [int(a) for a in arena.replay_arrays(kinds, values)]
+    allocations in order.  Does not reset (reference arena.py:325-340).
+    Events before an unknown kind are applied before it raises, as in the
+    reference's event-by-event loop."""
+    bad = next((i for i, ev in enumerate(events) if ev.kind not in _KIND), None)
+    kinds, values = encode_events(events if bad is None else events[:bad])
+    out = [int(a) for a in arena.replay_arrays(kinds, values)]
+    if bad is not None:
+        raise MemplanError(f"unknown event kind {events[bad].kind!r}")
+    return out
 
 
 def simulate_pool(events, pool: PoolAllocator | None = None) -> PoolAllocator:

@@ -92,7 +92,16 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
             MP_CUDA(cudaMemcpyAsync(s_d, size, nb, cudaMemcpyHostToDevice, s));
         }
     }
-    MP_TRY(plan_device(tp_d, tp_h.data(), T, a_d, f_d, s_d, o_d, p_d, flags, device, s));
+    {
+        const int rc = plan_device(tp_d, tp_h.data(), T, a_d, f_d, s_d, o_d, p_d, flags, device, s);
+        if (rc != MP_OK) {
+            // an early error return may leave the staged upload in flight:
+            // the next call on this thread must not overwrite its source
+            cudaStreamSynchronize(s);
+            cudaGetLastError();
+            return rc;
+        }
+    }
     if (stage) {
         // the staging buffer's input part was consumed by the upload above
         // (plan_device synchronised the stream)

@@ -143,3 +143,35 @@ def test_arena_ns_per_alloc():
                                   ctypes.byref(ns)) == 0
     print("arena ns/alloc", ns.value)
     assert ns.value < 200
+
+
+def test_fallback_is_a_full_pool_allocator():
+    """Arena.fallback is the arena's own PoolAllocator (arena.py:172): the
+    interrupted requests it served are visible through its full interface
+    (test_arena.py:66-71 reads .peak; cursor / live_bytes / alloc / free
+    complete the reference PoolAllocator surface)."""
+    inst = mp.build_instance([(4, 1, 3), (2, 2, 5), (3, 4, 6)])
+    arena = mp.Arena(mp.solve_bestfit(inst), inst)
+    arena.interrupt()
+    arena.alloc(9)
+    arena.resume()
+    fb = arena.fallback
+    assert isinstance(fb, mp.PoolAllocator)
+    assert fb.peak == 9 and fb.cursor == 9 and fb.live_bytes() == 9 and fb.last_ref == 1
+    addr = fb.alloc(5)
+    assert addr == 9 and fb.cursor == 14 and fb.live_bytes() == 14
+    fb.free(fb.last_ref)
+    assert fb.live_bytes() == 9
+    assert arena.peak_usage() == arena.plan.peak + fb.peak
+
+
+def test_replay_events_applies_prefix_before_unknown_kind():
+    """replay_events applies the events before an unknown kind, then raises
+    (the reference's event-by-event loop, arena.py:325-340)."""
+    inst = mp.build_instance([(4, 1, 3), (2, 2, 5), (3, 4, 6)])
+    arena = mp.Arena(mp.solve_bestfit(inst), inst)
+    bad = mp.TraceEvent("bogus")
+    events = [mp.alloc(4), mp.alloc(2), bad, mp.alloc(3)]
+    with pytest.raises(mp.MemplanError):
+        mp.replay_events(arena, events)
+    assert arena.lam == 3

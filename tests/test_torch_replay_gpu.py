@@ -30,6 +30,28 @@ def test_pluggable_allocator_replays_the_plan():
     assert out["hook_ns_per_alloc"] < 200
 
 
+def test_replay_safety_cases():
+    """Real-memory rules of csrc/torch_alloc.cpp: a tensor held across an
+    epoch boundary keeps its bytes; growth is side-served then re-planned on
+    the GPU at the next boundary into a larger region; a reordered free of a
+    grown block stops planned placement before it can alias; another stream
+    is side-served; tensors outlive replay_end and release the region last."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "torch_replay_cases.py")],
+                       capture_output=True, text=True, timeout=600)
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert lines, r.stderr[-3000:]
+    out = json.loads(lines[-1])
+    bad = [k for k, v in out.items() if isinstance(v, bool) and not v]
+    assert not bad, (bad, out)
+
+
+def test_floor_allocator_runs():
+    """torch's pluggable front end alone (trivial hooks): the floor under
+    the memplan hooks' through-torch cost."""
+    out = _run("floor")
+    assert out["ns_per_alloc"] > 0
+
+
 def test_caching_allocator_baseline_runs():
     out = _run("caching")
     assert out["ns_per_alloc"] > 0

@@ -11,6 +11,7 @@
 #include <c10/cuda/CUDACachingAllocator.h>
 
 #include <chrono>
+#include <cuda_runtime.h>
 #include <vector>
 
 // Returns (nanoseconds for the epoch, allocations outside [lo, lo + span)).
@@ -66,6 +67,26 @@ std::vector<int64_t> epoch_addresses(torch::Tensor kinds, torch::Tensor values) 
     for (void *p : ptrs)
         if (p) c10::cuda::CUDACachingAllocator::raw_delete(p);
     return out;
+}
+
+// Front-end floor of torch's CUDAPluggableAllocator: hooks that do nothing
+// but hand out distinct 512-byte-aligned addresses from a 64 MB ring (a
+// live set of up to 131072 allocations; the replayed epochs never touch the
+// memory).  Timing raw_alloc/raw_delete through these measures what torch's
+// pluggable front end costs by itself, the floor under memplan's hooks.
+extern "C" {
+static char *g_floor_base = nullptr;
+static uint64_t g_floor_next = 0;
+static const uint64_t kFloorSlots = 131072;
+void *floor_alloc(size_t size, int device, cudaStream_t stream) {
+    (void)size; (void)device; (void)stream;
+    if (!g_floor_base && cudaMalloc((void **)&g_floor_base, kFloorSlots * 512) != cudaSuccess)
+        return nullptr;
+    return g_floor_base + 512 * (g_floor_next++ % kFloorSlots);
+}
+void floor_free(void *ptr, size_t size, int device, cudaStream_t stream) {
+    (void)ptr; (void)size; (void)device; (void)stream;
+}
 }
 
 PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {

@@ -7,6 +7,15 @@ same size sequence served by
   caching   PyTorch's native CUDA caching allocator
   async     PyTorch's cudaMallocAsync backend
   carena    memplan's C-ABI arena alone (mp_arena_bench, no torch)
+  floor     a pluggable allocator whose hooks only hand out distinct
+            addresses (tools/replay/replay_ext.cpp floor_alloc/floor_free):
+            the cost of torch's CUDAPluggableAllocator front end itself,
+            i.e. the floor under any pluggable allocator
+
+Every torch allocator is timed twice: raw_alloc/raw_delete from C++
+(`ns_per_alloc`, the allocator path alone) and `torch.empty` from Python
+(`torch_empty_ns_per_alloc`, what a user's tensor creation costs end to
+end, Python dispatch included).
 
 The sequence is the hot cnn-like trace (GenSpec(model="cnn", layers=L,
 seed=0), reference cli.py:213 style), 2L allocations per epoch, all epochs
@@ -39,20 +48,49 @@ def _events(layers: int):
     return mp, events, kinds, values
 
 
+def _torch_empty_ns(torch, lib, kinds, values, reps: int) -> float:
+    """Best epoch of the same sequence as torch.empty(size, uint8) calls from
+    Python (tensor deleted at its free event): a user's end-to-end cost."""
+    import time
+    ev = list(zip(kinds.tolist(), values.tolist()))
+    n_alloc = sum(1 for k, _ in ev if k == 0)
+    best = float("inf")
+    empty, u8, dev = torch.empty, torch.uint8, torch.device("cuda")
+    for r in range(min(reps, 5) + 1):
+        if lib is not None:
+            assert lib.mp_torch_epoch_reset() == 0
+        live = []
+        t0 = time.perf_counter_ns()
+        for k, v in ev:
+            if k == 0:
+                live.append(empty(v, dtype=u8, device=dev))
+            elif k == 1:
+                live[v - 1] = None
+        t1 = time.perf_counter_ns()
+        live.clear()
+        if r:
+            best = min(best, t1 - t0)
+    return best / n_alloc
+
+
 def run_child(alloc: str, layers: int, reps: int) -> dict:
     import numpy as np
     if alloc == "async":
         os.environ["PYTORCH_CUDA_ALLOC_CONF"] = "backend:cudaMallocAsync"
     import torch
     from paper_1804_10001_b200 import _native as N
+    sys.path.insert(0, os.path.join(ROOT, "tools", "replay"))
+    from build_ext import BUILD, import_built
     if alloc == "memplan":
         pa = torch.cuda.memory.CUDAPluggableAllocator(N.LIB_PATH, "mp_torch_alloc",
                                                       "mp_torch_free")
         torch.cuda.memory.change_current_allocator(pa)
+    elif alloc == "floor":
+        pa = torch.cuda.memory.CUDAPluggableAllocator(
+            os.path.join(BUILD, "memplan_replay_ext.so"), "floor_alloc", "floor_free")
+        torch.cuda.memory.change_current_allocator(pa)
     torch.cuda.init()
     torch.empty(1, device="cuda")  # materialise the allocator for device 0
-    sys.path.insert(0, os.path.join(ROOT, "tools", "replay"))
-    from build_ext import import_built
     ext = import_built()
     mp, events, kinds, values = _events(layers)
     n_alloc = int((kinds == 0).sum())
@@ -97,6 +135,8 @@ def run_child(alloc: str, layers: int, reps: int) -> dict:
             outside = max(outside, outs)
     torch.cuda.synchronize()
     out["ns_per_alloc"] = best / n_alloc
+    out["torch_empty_ns_per_alloc"] = _torch_empty_ns(torch, lib if alloc == "memplan" else None,
+                                                      kinds, values, reps)
     if alloc == "memplan":
         # placement check: the replayed addresses are exactly base + offset
         assert lib.mp_torch_epoch_reset() == 0
@@ -112,7 +152,7 @@ def run_child(alloc: str, layers: int, reps: int) -> dict:
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--alloc", default="all", choices=["all", "memplan", "caching", "async",
-                                                      "carena"])
+                                                      "carena", "floor"])
     p.add_argument("--layers", type=int, default=5000)
     p.add_argument("--reps", type=int, default=20)
     args = p.parse_args()
@@ -120,7 +160,7 @@ def main():
         print(json.dumps(run_child(args.alloc, args.layers, args.reps)), flush=True)
         return
     res = {}
-    for a in ("carena", "memplan", "caching", "async"):
+    for a in ("carena", "memplan", "floor", "caching", "async"):
         r = subprocess.run([sys.executable, os.path.abspath(__file__), "--alloc", a, "--layers",
                             str(args.layers), "--reps", str(args.reps)],
                            capture_output=True, text=True, timeout=600)

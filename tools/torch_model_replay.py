@@ -18,7 +18,6 @@ the same iteration, so the two peaks can be compared.
 from __future__ import annotations
 
 import argparse
-import ctypes
 import json
 import os
 import subprocess
@@ -57,13 +56,10 @@ def iteration(torch, model, x, y):
 
 def run(alloc: str, batch: int, width: int, iters: int) -> dict:
     import torch
-    from paper_1804_10001_b200 import _native as N
-    lib = None
+    replay = None
     if alloc == "memplan":
-        pa = torch.cuda.memory.CUDAPluggableAllocator(N.LIB_PATH, "mp_torch_alloc",
-                                                      "mp_torch_free")
-        torch.cuda.memory.change_current_allocator(pa)
-        lib = N.lib()
+        from paper_1804_10001_b200.torch_replay import TorchReplay
+        replay = TorchReplay.install(alignment=512)
     torch.backends.cudnn.benchmark = False
     torch.backends.cudnn.deterministic = True
     torch.use_deterministic_algorithms(True, warn_only=True)
@@ -97,53 +93,45 @@ def run(alloc: str, batch: int, width: int, iters: int) -> dict:
     # reference iteration in passthrough mode (cudaMalloc per tensor)
     ref_loss, ref_grad = iteration(torch, model, x, y)
     torch.cuda.synchronize()
-    # record one iteration
-    assert lib.mp_torch_set_mode(1, None) == 0
-    iteration(torch, model, x, y)
-    torch.cuda.synchronize()
-    n = ctypes.c_int64()
-    lib.mp_torch_get_trace(None, None, 0, ctypes.byref(n))
-    kinds = np.zeros(n.value, np.int32)
-    values = np.zeros(n.value, np.int64)
-    lib.mp_torch_get_trace(N.ptr(kinds), N.ptr(values), n.value, ctypes.byref(n))
-    assert lib.mp_torch_set_mode(0, None) == 0
+    # record one iteration (profiler.py clock discipline over the hooks)
+    with replay.recording():
+        iteration(torch, model, x, y)
     if os.environ.get("MEMPLAN_SAVE_TRACE"):
+        kinds = np.array([0 if e.kind == "alloc" else 1 for e in replay.events], np.int32)
+        values = np.array([e.size if e.kind == "alloc" else e.ref for e in replay.events])
         np.savez(os.environ["MEMPLAN_SAVE_TRACE"], kinds=kinds, values=values)
-    events = [mp.alloc(int(v)) if k == 0 else mp.free(int(v)) for k, v in zip(kinds, values)]
-    inst = mp.profile_to_instance(mp.record(events), alignment=512)
     t0 = time.perf_counter()
-    plan = mp.solve_bestfit(inst)
+    plan = replay.plan()  # GPU planner
     out["plan_ms"] = 1e3 * (time.perf_counter() - t0)
-    out["trace_events"] = int(n.value)
+    inst = replay.instance
+    out["trace_events"] = len(replay.events)
     out["planned_blocks"] = len(inst.blocks)
     out["plan_peak_bytes"] = plan.peak
     out["clique_lower_bound_bytes"] = mp.clique_lower_bound(inst)
-    out["pool_peak_bytes"] = mp.simulate_pool(events).peak
-    arena = mp.Arena(plan, inst, base=0)
-    base = ctypes.c_uint64()
-    assert lib.mp_torch_replay_begin(arena._h, 0, ctypes.byref(base)) == 0
+    out["pool_peak_bytes"] = mp.simulate_pool(replay.events).peak
+    replay.begin()
     # replay: each iteration is one epoch of the arena
     equal = True
     for _ in range(2):
-        assert lib.mp_torch_epoch_reset() == 0
+        replay.new_epoch()
         lv, g = iteration(torch, model, x, y)
         torch.cuda.synchronize()
         equal = equal and bool(torch.equal(lv, ref_loss) and torch.equal(g, ref_grad))
         del lv, g
     t0 = time.perf_counter()
     for _ in range(iters):
-        assert lib.mp_torch_epoch_reset() == 0
+        replay.new_epoch()
         iteration(torch, model, x, y)
     torch.cuda.synchronize()
     out["ms_per_iteration"] = 1e3 * (time.perf_counter() - t0) / iters
-    planned, side, diverged = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-    lib.mp_torch_stats(ctypes.byref(planned), ctypes.byref(side), ctypes.byref(diverged))
-    out["requests_from_plan"] = planned.value
-    out["requests_outside_plan"] = side.value
-    out["epochs_off_profile"] = diverged.value
+    st = replay.stats()
+    out["requests_from_plan"] = st["n_planned"]
+    out["requests_outside_plan"] = st["n_side"]
+    out["epochs_off_profile"] = st["n_diverged"]
+    out["replans"] = st["n_replans"]
     out["replay_bit_identical"] = equal
-    assert lib.mp_torch_epoch_reset() == 0
-    assert lib.mp_torch_replay_end() == 0
+    replay.new_epoch()
+    replay.end()
     return out
 
 
