@@ -119,11 +119,14 @@ def _sha(a) -> str:
 
 
 def golden_huge() -> dict:
-    try:
-        with open(os.path.join(ROOT, "tests", "golden", "huge.json")) as fh:
-            return {c["name"]: c for c in json.load(fh)["cases"]}
-    except (OSError, ValueError, KeyError):
-        return {}
+    out = {}
+    for name in ("huge.json", "huge_lstm.json"):
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", name)) as fh:
+                out.update({c["name"]: c for c in json.load(fh)["cases"]})
+        except (OSError, ValueError, KeyError):
+            pass
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -424,7 +427,7 @@ def config_suite(cpu_procs: int, sweep_1e6: bool) -> dict:
         wall, (off, pks) = _best_wall(lambda: solve_bestfit_batched_arrays(tp, A, F, S), 5)
         info = plan_info()
         exact = oracle_check(tp, A, F, S, off, pks, range(len(tp) - 1), cpu_procs)
-        g = gold.get(f"lstm_L{layers}")
+        g = gold.get(f"lstm_L{layers}_a{ALIGN}")
         cols = [(A[tp[t]:tp[t + 1]], F[tp[t]:tp[t + 1]], S[tp[t]:tp[t + 1]])
                 for t in range(len(tp) - 1)]
         chunks = [cols[i::cpu_procs] for i in range(cpu_procs)]

@@ -74,21 +74,23 @@ def solve_one(name: str) -> dict:
             "ref_s": round(dt, 2)}
 
 
-def lstm_one(layers: int) -> dict:
+def lstm_one(layers: int, alignment: int = 1) -> dict:
     """All 4096 profiles of BASELINE.json config 4 (workloads.py:74-126)."""
     import memplan as M
     spec = M.GenSpec(model="rnn", layers=layers, batch=64, seed=2024, variable_length=(10, 50))
     peaks, offs, rows, ns = [], [], [], []
     t0 = time.perf_counter()
     for ell in M.rnn_epoch_lengths(spec, 4096):
-        inst = M.profile_to_instance(M.record(M.parse_trace(M.rnn_like_trace(spec, ell))))
+        inst = M.profile_to_instance(M.record(M.parse_trace(M.rnn_like_trace(spec, ell))),
+                                     alignment=alignment)
         plan = M.solve_bestfit(inst)
         peaks.append(plan.peak)
         ns.append(len(inst.blocks))
         offs.extend(plan.offsets[b.id] for b in inst.blocks)
         rows.extend([b.size, b.alloc_time, b.free_time] for b in inst.blocks)
     dt = time.perf_counter() - t0
-    return {"name": f"lstm_L{layers}", "profiles": 4096, "blocks_total": int(sum(ns)),
+    return {"name": f"lstm_L{layers}" + (f"_a{alignment}" if alignment != 1 else ""),
+            "alignment": alignment, "profiles": 4096, "blocks_total": int(sum(ns)),
             "n_per_profile": sorted(set(ns)),
             "blocks_sha256": _sha(np.array(rows, np.int64)),
             "offsets_sha256": _sha(np.array(offs, np.int64)),
@@ -99,11 +101,12 @@ def lstm_one(layers: int) -> dict:
 
 def run(job: str) -> dict:
     if job.startswith("lstm_L"):
-        return lstm_one(int(job[6:]))
+        parts = job[6:].split("_a")
+        return lstm_one(int(parts[0]), int(parts[1]) if len(parts) > 1 else 1)
     return solve_one(job)
 
 
-JOBS = ["lstm_L6", "lstm_L64",
+JOBS = ["lstm_L6", "lstm_L64", "lstm_L6_a512", "lstm_L64_a512",
         "uniform_1e5_s0", "cnn_1e5_s0", "walk_1e5_s0", "uniform_1e5_s1", "walk_1e5_s1",
         "cnn_1e6_s0", "uniform_1e6_s0"]
 
@@ -112,11 +115,12 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--jobs", type=int, default=7)
     ap.add_argument("--only", default="")
+    ap.add_argument("--out", default=OUT)
     args = ap.parse_args()
     jobs = [j for j in JOBS if not args.only or j in args.only.split(",")]
     done = {}
-    if os.path.exists(OUT):
-        with open(OUT) as fh:
+    if os.path.exists(args.out):
+        with open(args.out) as fh:
             done = {c["name"]: c for c in json.load(fh)["cases"]}
     jobs = [j for j in jobs if j not in done]
     # the 10^6 solves first: they bound the wall time
@@ -125,7 +129,7 @@ def main() -> None:
         for res in pool.imap_unordered(run, jobs):
             done[res["name"]] = res
             print(json.dumps(res), flush=True)
-            with open(OUT, "w") as fh:
+            with open(args.out, "w") as fh:
                 json.dump({"generator": "tests/golden/make_huge_golden.py (reference memplan)",
                            "cases": [done[k] for k in sorted(done)]}, fh, indent=1)
 

@@ -29,7 +29,9 @@ def test_bench_json_contract_single_gpu():
               "gpu_launches", "roofline", "cpu_baseline", "clocks"):
         assert k in d, k
     assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0
-    assert d["parity_trace0_vs_oracle"] is True
+    assert d["parity_vs_oracle"]["bit_exact"] is True
+    assert d["parity_vs_oracle"]["traces_checked"] >= 16
+    assert d["roofline"]["bound"] == "latency" and 0 < d["roofline"]["frac"] <= 1.2
     assert set(d["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
     assert set(d["roofline"]) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
 
@@ -43,3 +45,29 @@ def test_bench_two_ranks_one_gpu():
     d = _last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["config"]["global_batch_traces"] == 128
+    assert d["parity_vs_oracle"]["gathered_bit_exact"] is True
+
+
+def test_bench_lstm_two_ranks_one_gpu():
+    """configs[3] through dist.lpt_shards + gather_device with the GPU
+    planner on every rank; rank 0 checks all 4096 gathered profiles against
+    the C oracle."""
+    env = dict(os.environ, MEMPLAN_BENCH_BACKEND="gloo", MEMPLAN_BENCH_DEVICE="0")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--workload", "lstm", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    d = _last_json(r.stdout)
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["parity_vs_oracle"]["bit_exact"] is True
+    assert d["parity_vs_oracle"]["gathered_bit_exact"] is True
+
+
+def test_bench_reference_arm_times_the_reference():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "1", "--blocks", "2000"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    d = _last_json(r.stdout)
+    assert d["impl"] == "reference"
+    assert d["cpu_baseline"]["kind"] == "reference" and d["value"] > 0
