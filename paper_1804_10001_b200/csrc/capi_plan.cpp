@@ -1,6 +1,8 @@
 // extern "C" planning entry points (include/memplan_b200.h).
 #include <string.h>
 
+#include <algorithm>
+
 #include <vector>
 
 #include "common.h"
@@ -67,14 +69,27 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
     const size_t nb = sizeof(int64_t) * (size_t)N;
     const size_t in_b = sizeof(int64_t) * (size_t)(T + 1) + 3 * nb;
     const size_t out_b = nb + sizeof(int64_t) * (size_t)T;
+    // small plans reuse this thread's device workspace (no allocation); the
+    // planner carves its own tables from a separate per-thread buffer
+    int64_t *stage = (in_b <= kStageBytes && out_b <= kStageBytes) ? pinned_stage(device) : nullptr;
     Scratch buf;
-    MP_TRY(buf.alloc(in_b + out_b + 256, s));
-    int64_t *tp_d = buf.as<int64_t>();
+    int64_t *tp_d;
+    if (stage) {
+        static thread_local Scratch io[64];
+        Scratch &w = io[device];
+        if (w.bytes < in_b + out_b + 256 || w.stream != s) {
+            if (w.ptr) cudaStreamSynchronize(w.stream);
+            MP_TRY(w.alloc(std::max(in_b + out_b + 256, w.bytes + w.bytes / 2), s));
+        }
+        tp_d = w.as<int64_t>();
+    } else {
+        MP_TRY(buf.alloc(in_b + out_b + 256, s));
+        tp_d = buf.as<int64_t>();
+    }
     int64_t *a_d = tp_d + (T + 1), *f_d = a_d + N, *s_d = f_d + N;
     int64_t *o_d = s_d + N, *p_d = o_d + N;
     // small plans (per-network planning) go through a pinned staging buffer:
     // two copies instead of six pageable ones
-    int64_t *stage = (in_b <= kStageBytes && out_b <= kStageBytes) ? pinned_stage(device) : nullptr;
     if (stage) {
         memcpy(stage, tp_h.data(), sizeof(int64_t) * (T + 1));
         if (N) {
@@ -92,8 +107,11 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
             MP_CUDA(cudaMemcpyAsync(s_d, size, nb, cudaMemcpyHostToDevice, s));
         }
     }
+    // staged plans: the results' copy rides the planner's own synchronisation
+    HostCopy hc{stage, o_d, out_b, false};
     {
-        const int rc = plan_device(tp_d, tp_h.data(), T, a_d, f_d, s_d, o_d, p_d, flags, device, s);
+        const int rc = plan_device(tp_d, tp_h.data(), T, a_d, f_d, s_d, o_d, p_d, flags, device, s,
+                                   stage ? &hc : nullptr);
         if (rc != MP_OK) {
             // an early error return may leave the staged upload in flight:
             // the next call on this thread must not overwrite its source
@@ -105,8 +123,10 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
     if (stage) {
         // the staging buffer's input part was consumed by the upload above
         // (plan_device synchronised the stream)
-        MP_CUDA(cudaMemcpyAsync(stage, o_d, out_b, cudaMemcpyDeviceToHost, s));
-        MP_CUDA(cudaStreamSynchronize(s));
+        if (!hc.done) {
+            MP_CUDA(cudaMemcpyAsync(stage, o_d, out_b, cudaMemcpyDeviceToHost, s));
+            MP_CUDA(cudaStreamSynchronize(s));
+        }
         if (N) memcpy(offsets_out, stage, nb);
         if (T) memcpy(peaks_out, stage + N, sizeof(int64_t) * T);
         return MP_OK;

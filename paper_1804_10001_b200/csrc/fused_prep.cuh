@@ -18,6 +18,7 @@ constexpr int kFusedMaxThreads = 256;
 
 struct FusedIn {
     const int64_t *alloc, *free_, *size;  // batch columns (device)
+    uint2 *ent;                           // window entries in (alloc, id) order (TIER_WARP)
     int64_t *unit, *tmin, *tspan;         // per trace outputs
     uint64_t *total_units;
     uint32_t *U;
@@ -226,6 +227,7 @@ __device__ void prep_small(const int64_t *trace_ptr, const FusedIn &in, uint32_t
         rec[b + pr] = r;
         raw2[b + pr] = make_uint2((uint32_t)(A[i] - tmin), (uint32_t)(F[i] - tmin));
         sh.ent[r.pos] = make_uint2(r.frank, pr);
+        in.ent[b + r.pos] = make_uint2(r.frank, pr);
     }
     if (tid == 0) in.U[t] = sh.U;
     __syncthreads();

@@ -71,7 +71,8 @@ constexpr int kPendCap = 128;
 // + chunk skeleton / + chunk-sorted table.
 // TIER_SCAN: small traces keep the table in shared memory and scan their
 // (short) windows row by row — no skeletons to maintain at all.
-enum { TIER_GLOBAL = 0, TIER_GROUP = 1, TIER_SKEL = 2, TIER_ALL = 3, TIER_SCAN = 4 };
+enum { TIER_GLOBAL = 0, TIER_GROUP = 1, TIER_SKEL = 2, TIER_ALL = 3, TIER_SCAN = 4,
+       TIER_WARP = 5 /* TIER_TINY, warp_engine.cuh; host-side label only */ };
 // Flagged groups evaluated per memory round, and pending segments read per
 // lane per wave.  Single traces: 4 groups with the chunk skeletons in shared
 // memory (tier SKEL), else 3, and 2 segments.  LEAN (the batched kernel
@@ -1036,6 +1037,22 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
     }
 }
 
+}  // namespace
+}  // namespace mp
+#include "warp_engine.cuh"
+namespace mp {
+namespace {
+
+// TIER_TINY planner: one warp per trace (grid = traces or tlist); packed
+// choose keys when every height fits 27 bits
+template <bool STATS>
+__global__ void __launch_bounds__(32) k_tiny(PlanArgs a, const uint2 *ent, int packed) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int t = a.tlist ? a.tlist[blockIdx.x] : (int)blockIdx.x;
+    if (packed) plan_tiny<true, STATS>(a, ent, t, smem);
+    else plan_tiny<false, STATS>(a, ent, t, smem);
+}
+
 template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER, bool TIMING>
 __global__ void __launch_bounds__(32 * NW) k_plan(PlanArgs a) {
     plan_trace<HT, LINES_SMEM, STATS, NW, TIER, TIMING>(a, a.tlist ? a.tlist[blockIdx.x]
@@ -1059,7 +1076,11 @@ __global__ void __launch_bounds__(32, kOccCtas) k_plan_occ(PlanArgs a) {
 // memory (prep_small), then its warp 0 runs the TIER_SCAN step loop.
 // One-warp CTAs (<= 128 blocks) are capped at 128 registers (no spill), so
 // 16 traces share an SM (LSTM 4096 profiles: 0.118 -> 0.094 ms).
-template <int THREADS, int ITEMS, bool STATS>
+// The step loop is TIER_TINY (warp_engine.cuh) for 32-bit heights — a trace
+// whose skyline outgrows its 31 register lines restarts right here on
+// plan_trace TIER_SCAN — and TIER_SCAN for 64-bit heights (TINY = 0:
+// TIER_SCAN only, the pre-r2 loop kept for A/B runs).
+template <int THREADS, int ITEMS, bool STATS, int TINY>
 __global__ void __launch_bounds__(THREADS, THREADS == 32 ? 16 : 1) k_fused_small(PlanArgs a, FusedIn in) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int t = (int)blockIdx.x;
@@ -1068,10 +1089,17 @@ __global__ void __launch_bounds__(THREADS, THREADS == 32 ? 16 : 1) k_fused_small
         prep_small<THREADS, ITEMS>(a.trace_ptr, in, a.sf, a.sp, const_cast<Rec *>(a.rec),
                           const_cast<uint2 *>(a.raw2), t, smem);
     if (threadIdx.x >= 32) return;
-    if (n == 0 || in.total_units[t] < (uint64_t(1) << 32))
-        plan_trace<uint32_t, true, STATS, 1, TIER_SCAN, false, true>(a, t);
-    else
+    if (n == 0 || in.total_units[t] < (uint64_t(1) << 32)) {
+        int st = PS_LINES_OVERFLOW;
+        if constexpr (TINY > 0) {
+            st = in.total_units[t] < (uint64_t(1) << 27) ? plan_tiny<true, STATS>(a, in.ent, t, smem)
+                                                         : plan_tiny<false, STATS>(a, in.ent, t, smem);
+            __syncwarp();
+        }
+        if (st == PS_LINES_OVERFLOW) plan_trace<uint32_t, true, STATS, 1, TIER_SCAN, false, true>(a, t);
+    } else {
         plan_trace<uint64_t, true, STATS, 1, TIER_SCAN, false, true>(a, t);
+    }
 }
 
 constexpr int64_t kFusedMaxBlocks = 2048;
@@ -1128,6 +1156,52 @@ thread_local bool g_occ = false;   // batched launch: use the register-capped k_
 // cannot lower each other's shared-memory opt-in between set and launch.
 std::mutex g_launch_mu;
 
+int sm_count(int device) {
+    static int cache[64] = {0};
+    int v = device >= 0 && device < 64 ? cache[device] : 0;
+    if (!v) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+        if (device >= 0 && device < 64) cache[device] = v;
+    }
+    return v > 0 ? v : 148;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when the value for
+// this kernel changes (a driver call per plan otherwise); callers hold
+// g_launch_mu
+struct AttrCache {
+    const void *fn;
+    int smem;
+};
+int set_smem_attr(const void *fn, int smem) {
+    static AttrCache cache[64];
+    static int used = 0;
+    for (int i = 0; i < used; i++)
+        if (cache[i].fn == fn) {
+            if (cache[i].smem == smem) return MP_OK;
+            MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            cache[i].smem = smem;
+            return MP_OK;
+        }
+    MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (used < 64) cache[used++] = AttrCache{fn, smem};
+    return MP_OK;
+}
+
+// per-thread events and a pinned reduced-stats buffer for the fused path
+struct FusedCtx {
+    cudaEvent_t k0 = nullptr, k1 = nullptr;
+    int64_t *red_h = nullptr;
+    int init() {
+        if (k0) return MP_OK;
+        MP_CUDA(cudaEventCreate(&k0));
+        MP_CUDA(cudaEventCreate(&k1));
+        MP_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&red_h), 256, cudaHostAllocDefault));
+        return MP_OK;
+    }
+};
+thread_local FusedCtx g_fctx;
+
 template <typename HT, bool Ls, bool ST, int NW, int TIER, bool TM>
 int launch_kt(const PlanArgs &a, int grid, size_t smem, cudaStream_t s) {
     auto fn = k_plan<HT, Ls, ST, NW, TIER, TM>;
@@ -1181,6 +1255,17 @@ int launch_ht(const PlanArgs &a, int grid, int tier, bool lines_smem, size_t sme
     return launch_tier<HT, false, ST>(a, grid, tier, smem, s);
 }
 
+int launch_tiny(const PlanArgs &a, const uint2 *ent, int grid, size_t smem, bool stats,
+                bool packed, cudaStream_t s) {
+    auto fn = stats ? k_tiny<true> : k_tiny<false>;
+    std::lock_guard<std::mutex> lock(g_launch_mu);
+    MP_TRY(set_smem_attr(reinterpret_cast<const void *>(fn), (int)smem));
+    fn<<<grid, 32, smem, s>>>(a, ent, packed ? 1 : 0);
+    MP_CUDA(cudaGetLastError());
+    g_launches++;
+    return MP_OK;
+}
+
 int launch_plan(const PlanArgs &a, int grid, bool h32, int tier, bool lines_smem, size_t smem,
                 cudaStream_t s, bool stats) {
     if (stats)
@@ -1193,10 +1278,16 @@ int launch_plan(const PlanArgs &a, int grid, bool h32, int tier, bool lines_smem
 thread_local mp_plan_info g_info;
 
 size_t smem_limit(int device) {
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    static int cache[64] = {0};
+    int v = device >= 0 && device < 64 ? cache[device] : 0;
+    if (!v) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        if (device >= 0 && device < 64) cache[device] = v;
+    }
     return v > 0 ? (size_t)v : 48 * 1024;
 }
+
+
 
 inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -1265,6 +1356,20 @@ Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwar
 
 const mp_plan_info &last_plan_info() { return g_info; }
 
+void *plan_workspace(size_t bytes, cudaStream_t s) {
+    // one per thread and device; grown (never shrunk) on demand
+    static thread_local Scratch ws[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    Scratch &w = ws[dev];
+    if (w.bytes < bytes || w.stream != s) {
+        if (w.ptr) cudaStreamSynchronize(w.stream);  // no plan still reads it
+        if (w.alloc(std::max(bytes, w.bytes + w.bytes / 2), s) != MP_OK) return nullptr;
+    }
+    return w.ptr;
+}
+
 namespace {
 
 // Fold per-trace planner statistics into g_info; map the status words to the
@@ -1296,16 +1401,25 @@ int collect_stats(const std::vector<int64_t> &hst, int64_t T) {
 
 constexpr int kFusedFallback = -1;
 
-template <int THREADS, int ITEMS>
-int launch_fused(const PlanArgs &a, const FusedIn &in, int grid, size_t smem, bool stats,
-                 cudaStream_t s) {
-    auto fn = stats ? k_fused_small<THREADS, ITEMS, true> : k_fused_small<THREADS, ITEMS, false>;
+template <int THREADS, int ITEMS, int TINY>
+int launch_fused_l(const PlanArgs &a, const FusedIn &in, int grid, size_t smem, bool stats,
+                   cudaStream_t s) {
+    auto fn = stats ? k_fused_small<THREADS, ITEMS, true, TINY>
+                    : k_fused_small<THREADS, ITEMS, false, TINY>;
     std::lock_guard<std::mutex> lock(g_launch_mu);
-    MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MP_TRY(set_smem_attr(reinterpret_cast<const void *>(fn), (int)smem));
     fn<<<grid, THREADS, smem, s>>>(a, in);
     MP_CUDA(cudaGetLastError());
     g_launches++;
     return MP_OK;
+}
+
+// tiny = 0: the TIER_SCAN loop (A/B runs, MEMPLAN_NO_TINY)
+template <int THREADS, int ITEMS>
+int launch_fused(const PlanArgs &a, const FusedIn &in, int grid, size_t smem, bool stats,
+                 int tiny, cudaStream_t s) {
+    if (tiny) return launch_fused_l<THREADS, ITEMS, 1>(a, in, grid, smem, stats, s);
+    return launch_fused_l<THREADS, ITEMS, 0>(a, in, grid, smem, stats, s);
 }
 
 // Traces of at most kFusedMaxBlocks blocks: one launch, no global sorts and
@@ -1314,7 +1428,8 @@ int launch_fused(const PlanArgs &a, const FusedIn &in, int grid, size_t smem, bo
 // caller then takes the general path, which restarts such traces).
 int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
                const int64_t *alloc_d, const int64_t *free_d, const int64_t *size_d,
-               int64_t *offsets_d, int64_t *peaks_d, int flags, int device, cudaStream_t s) {
+               int64_t *offsets_d, int64_t *peaks_d, int flags, int device, cudaStream_t s,
+               HostCopy *hc) {
     if (nmax > kFusedMaxBlocks || (flags & MP_FORCE_GLOBAL) || getenv("MEMPLAN_NO_FUSED"))
         return kFusedFallback;
     // CTA shape by size: one warp (the planner's own) for tiny traces, so the
@@ -1325,8 +1440,7 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
                            : variant == 1 ? sizeof(SmallPrep<128, 8>::Shared)
                                           : sizeof(SmallPrep<256, 16>::Shared);
     // planner layout (TIER_SCAN), sized for 64-bit heights so either fits
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int sms = sm_count(device);
     const size_t lim = smem_limit(device) - 8192;  // two StepShared blocks + prep statics
     const int conc = (int)std::min<int64_t>((T + sms - 1) / sms, 8);
     const size_t budget = conc > 1 ? std::min(lim, (size_t)(228 * 1024) / conc - 8192) : lim;
@@ -1334,17 +1448,21 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     const int lcap = (int)std::min<int64_t>(lneed, conc > 1 ? 256 : 1024);
     Layout lay = choose_layout(nmax, lcap, 8, budget, 1, false);
     if (lay.tier != TIER_SCAN || !lay.lines_smem) return kFusedFallback;
-    const size_t smem = std::max(prep_smem + 256, lay.smem);
+    // step loop: TIER_WARP (register skyline) unless disabled (A/B runs)
+    const int tiny = getenv("MEMPLAN_NO_TINY") ? 0 : 1;
+    const size_t smem = std::max(std::max(prep_smem + 256, lay.smem),
+                                 tiny ? tiny_smem_bytes(nmax) : size_t(0));
     if (smem > lim) return kFusedFallback;
 
     const int64_t nchunks = N / 32 + T + 1;
     const size_t bytes = 2 * Carver::need<uint32_t>(32 * nchunks) + Carver::need<Rec>(N) +
-                         Carver::need<uint2>(N) + Carver::need<uint32_t>(T) +
+                         2 * Carver::need<uint2>(N) + Carver::need<uint32_t>(T) +
                          4 * Carver::need<int64_t>(T) + Carver::need<int64_t>(T * ST_N) +
                          Carver::need<int64_t>(ST_N + 2);
-    Scratch sc;
-    MP_TRY(sc.alloc(bytes, s));
-    Carver cv(sc.ptr, bytes);
+    void *ws = plan_workspace(bytes, s);
+    if (!ws) return MP_ERR_CUDA;
+    MP_TRY(g_fctx.init());
+    Carver cv(ws, bytes);
     PlanArgs a{};
     FusedIn in{};
     a.trace_ptr = trace_ptr_d;
@@ -1354,6 +1472,7 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     uint2 *raw2 = cv.take<uint2>(N);
     a.rec = rec;
     a.raw2 = raw2;
+    in.ent = cv.take<uint2>(N);
     in.U = cv.take<uint32_t>(T);
     in.unit = cv.take<int64_t>(T);
     in.tmin = cv.take<int64_t>(T);
@@ -1373,37 +1492,33 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     a.lcap = lcap;
     a.rec_smem = lay.rec_smem;
     const bool stats_on = (flags & MP_STATS) != 0;
-    cudaEvent_t k0, k1;
-    cudaEventCreate(&k0);
-    cudaEventCreate(&k1);
+    cudaEvent_t k0 = g_fctx.k0, k1 = g_fctx.k1;
     const int64_t launches0 = g_launches;
     cudaEventRecord(k0, s);
-    int rc = variant == 0 ? launch_fused<32, 8>(a, in, (int)T, smem, stats_on, s)
-           : variant == 1 ? launch_fused<128, 8>(a, in, (int)T, smem, stats_on, s)
-                          : launch_fused<256, 16>(a, in, (int)T, smem, stats_on, s);
-    if (rc != MP_OK) {
-        cudaEventDestroy(k0);
-        cudaEventDestroy(k1);
-        return rc;
-    }
+    int rc = variant == 0 ? launch_fused<32, 8>(a, in, (int)T, smem, stats_on, tiny, s)
+           : variant == 1 ? launch_fused<128, 8>(a, in, (int)T, smem, stats_on, tiny, s)
+                          : launch_fused<256, 16>(a, in, (int)T, smem, stats_on, tiny, s);
+    if (rc != MP_OK) return rc;
     cudaEventRecord(k1, s);
     k_reduce_stats<<<1, kRedThreads, 0, s>>>(stats, T, red);
     MP_CUDA(cudaGetLastError());
     g_launches++;
-    std::vector<int64_t> hst(ST_N + 2);
-    MP_CUDA(cudaMemcpyAsync(hst.data(), red, sizeof(int64_t) * (ST_N + 2), cudaMemcpyDeviceToHost,
-                            s));
+    // host-array callers: their results ride the same round trip
+    if (hc) MP_CUDA(cudaMemcpyAsync(hc->dst, hc->src, hc->bytes, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(g_fctx.red_h, red, sizeof(int64_t) * (ST_N + 2),
+                            cudaMemcpyDeviceToHost, s));
     MP_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> hst(g_fctx.red_h, g_fctx.red_h + ST_N + 2);
     float ms = 0;
     cudaEventElapsedTime(&ms, k0, k1);
-    cudaEventDestroy(k0);
-    cudaEventDestroy(k1);
     if (hst[ST_N] > 0) return kFusedFallback;
+    if (hc) hc->done = true;
     g_info.prep_ms = 0;
     g_info.plan_ms = ms;
     g_info.kernel_ms = ms;
     g_info.launches = g_launches - launches0;
-    g_info.engine = 8 | 2 | (lay.rec_smem ? 1 : 0) | 128 | 256;  // 256: fused small-trace path
+    // 256: fused small-trace path; 512: TIER_TINY step loop
+    g_info.engine = 8 | 2 | (lay.rec_smem ? 1 : 0) | 128 | 256 | (tiny ? 512 : 0);
     g_info.cluster = 1;
     return collect_stats(hst, 1);
 }
@@ -1412,7 +1527,8 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
 
 int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t T,
                 const int64_t *alloc_d, const int64_t *free_d, const int64_t *size_d,
-                int64_t *offsets_d, int64_t *peaks_d, int flags, int device, cudaStream_t s) {
+                int64_t *offsets_d, int64_t *peaks_d, int flags, int device, cudaStream_t s,
+                HostCopy *hc) {
     g_info = mp_plan_info{};
     if (T <= 0) return MP_OK;
     const int64_t N = trace_ptr_h[T] - trace_ptr_h[0];
@@ -1428,7 +1544,7 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     }
     {
         const int rc = plan_fused(trace_ptr_d, T, N, nmax, alloc_d, free_d, size_d, offsets_d,
-                                  peaks_d, flags, device, s);
+                                  peaks_d, flags, device, s, hc);
         if (rc != kFusedFallback) return rc;
         g_info = mp_plan_info{};
     }
@@ -1496,8 +1612,7 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     // latency, so each CTA is budgeted 1/conc of the SM's shared memory
     // (conc = traces per SM, capped) and the window structures take the
     // highest tier that fits that budget.
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int sms = sm_count(device);
     // more than one trace per SM: the register-capped kernel, up to 16 per SM
     g_occ = T > sms;
     if (const char *env = getenv("MEMPLAN_OCC")) g_occ = atoi(env) != 0;
@@ -1564,7 +1679,21 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     cudaEvent_t k0, k1;
     cudaEventCreate(&k0); cudaEventCreate(&k1);
     cudaEventRecord(k0, s);
-    MP_TRY(launch_plan(a, (int)T, h32, lay.tier, lay.lines_smem, lay.smem, s, stats_on));
+    // TIER_TINY (register skyline, warp_engine.cuh) for traces of up to
+    // kTinyMaxBlocks blocks with 32-bit heights when no more traces than SMs;
+    // traces whose skyline outgrows the 31 register lines come back as
+    // PS_LINES_OVERFLOW and re-run below on plan_trace
+    bool h27 = true;
+    for (int64_t t = 0; t < T; t++) h27 = h27 && tot[t] < (uint64_t(1) << 27);
+    const bool use_tiny = h32 && nmax <= kTinyMaxBlocks && T <= sms && !force_global &&
+                          !a.timing && g_nwarps == 1 && !getenv("MEMPLAN_NO_TINY") &&
+                          !getenv("MEMPLAN_TIER") && tiny_smem_bytes(nmax) <= lim;
+    if (use_tiny) {
+        MP_TRY(launch_tiny(a, po.ent, (int)T, tiny_smem_bytes(nmax), stats_on, h27, s));
+        lay.tier = TIER_WARP;
+    } else {
+        MP_TRY(launch_plan(a, (int)T, h32, lay.tier, lay.lines_smem, lay.smem, s, stats_on));
+    }
     cudaEventRecord(k1, s);
 
     // ---- collect status; re-run overflowed traces with global lines ----
@@ -1610,12 +1739,12 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     g_info.plan_ms = ms_plan;
     g_info.kernel_ms = ms_kernel;
     g_info.launches = prep_launches() + (g_launches - launches0);
-    g_info.engine = (h32 ? 16 : 0) | (lay.lines_smem ? 8 : 0) |
-                    (lay.tier >= TIER_SKEL && lay.tier != TIER_SCAN ? 4 : 0) |
-                    (lay.tier >= TIER_ALL ? 2 : 0) | (lay.rec_smem ? 1 : 0) |
-                    (redo.empty() ? 0 : 32) |
-                    (lay.tier >= TIER_GROUP && lay.tier != TIER_SCAN ? 64 : 0) |
-                    (lay.tier == TIER_SCAN ? 128 : 0);
+    const bool skel = lay.tier != TIER_SCAN && lay.tier != TIER_WARP;
+    g_info.engine = (h32 ? 16 : 0) | (lay.lines_smem && lay.tier != TIER_WARP ? 8 : 0) |
+                    (skel && lay.tier >= TIER_SKEL ? 4 : 0) |
+                    (skel && lay.tier >= TIER_ALL ? 2 : 0) | (lay.rec_smem ? 1 : 0) |
+                    (redo.empty() ? 0 : 32) | (skel && lay.tier >= TIER_GROUP ? 64 : 0) |
+                    (lay.tier == TIER_SCAN ? 128 : 0) | (lay.tier == TIER_WARP ? 512 : 0);
     g_info.cluster = g_nwarps;  // warps per trace (single-CTA engine)
     return collect_stats(hst, T);
 }
