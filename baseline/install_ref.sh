@@ -13,3 +13,7 @@ python -m pip install --no-index --no-build-isolation --no-deps --find-links /op
     --target "$HERE/_ref" "$TMP/pkg"
 rm -rf "$TMP"
 PYTHONPATH="$HERE/_ref" python -c "import memplan; print('installed', memplan.__file__)"
+# the reference's own test suite, run against the drop-in on the GPU box by
+# tests/test_reference_suite_gpu.py (import alias tests/refsuite/memplan)
+rm -rf "$HERE/_ref/reftests"
+cp -r "$SRC/tests" "$HERE/_ref/reftests"

@@ -49,6 +49,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "common.h"
 #include "plan.h"
 #include "plan_types.cuh"
@@ -56,6 +58,8 @@
 #include "fused_prep.cuh"
 
 namespace mp {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -72,7 +76,8 @@ constexpr int kPendCap = 128;
 // TIER_SCAN: small traces keep the table in shared memory and scan their
 // (short) windows row by row — no skeletons to maintain at all.
 enum { TIER_GLOBAL = 0, TIER_GROUP = 1, TIER_SKEL = 2, TIER_ALL = 3, TIER_SCAN = 4,
-       TIER_WARP = 5 /* TIER_TINY, warp_engine.cuh; host-side label only */ };
+       TIER_WARP = 5 /* TIER_TINY, warp_engine.cuh; host-side label only */,
+       TIER_CLU = 6 /* TIER_SKEL in a cluster, table over DSMEM; host-side label */ };
 // Flagged groups evaluated per memory round, and pending segments read per
 // lane per wave.  Single traces: 4 groups with the chunk skeletons in shared
 // memory (tier SKEL), else 3, and 2 segments.  LEAN (the batched kernel
@@ -104,6 +109,8 @@ struct PlanArgs {
     int lcap;                 // line slots per trace (excluding sentinel)
     int rec_smem;             // winner records in shared memory
     int timing;               // diagnostics: per-phase clock() sums (NW = 1)
+    int clu_cshift, clu_pshift;  // cluster tier: chunks / priorities per worker CTA (log2)
+    const uint32_t *lt;       // cluster tier: N lifetimes (raw free - raw alloc), priority order
 };
 
 __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -172,7 +179,47 @@ struct Win {
     uint32_t *sf, *sp;   // chunk-sorted table (shared or global)
     uint32_t *cnt;       // live count per chunk (global, STATS only)
     uint64_t keep, stream;  // L2 policies (global tiers)
+    // cluster tier (CLU): the table and the per-priority lifetimes live in
+    // the shared memory of the cluster's worker CTAs (ranks 1..), read
+    // through DSMEM; placed entries are tracked in a per-chunk bitmap in the
+    // planner CTA's own shared memory (the remote table stays read-only)
+    uint32_t tab;        // shared::cta offset of each worker's slice
+    int cshift, pshift;  // chunks / priorities per worker: 1 << shift
+    uint32_t *dead;      // per chunk: bit p = position 32 j + p placed
 };
+
+// ---- DSMEM access (cluster tier) ----
+__device__ __forceinline__ uint32_t dsm_map(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ uint32_t dsm_ld(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 dsm_ld4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared::cluster.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a));
+    return v;
+}
+// cluster address of chunk j's SF row (its SP row follows the worker's SF
+// slice: + (128 << cshift))
+__device__ __forceinline__ uint32_t dsm_row(const Win &w, int j) {
+    const uint32_t jl = (uint32_t)j & ((1u << w.cshift) - 1u);
+    return dsm_map(w.tab + 128u * jl, 1u + ((uint32_t)j >> w.cshift));
+}
+__device__ __forceinline__ uint32_t dsm_lifetime(const Win &w, uint32_t prio) {
+    const uint32_t pl = prio & ((1u << w.pshift) - 1u);
+    return dsm_ld(dsm_map(w.tab + (256u << w.cshift) + 4u * pl, 1u + (prio >> w.pshift)));
+}
+// a placed entry reads as kDead
+__device__ __forceinline__ uint32_t dead_mask(uint32_t dm, uint32_t key, uint32_t pr) {
+    return (dm >> (key & 31u)) & 1u ? kDead : pr;
+}
 
 // L2 cache policies for the global-memory tiers: the group / S0 skeletons are
 // the hot, re-read working set of every step (evict_last); everything else
@@ -236,12 +283,18 @@ struct RetireRow {
     uint4 gq;  // S0 of chunk 32*(j>>5) + lane (the retired chunk's group)
 };
 
-template <bool SG, bool SCAN = false>
+template <bool SG, bool SCAN = false, bool CLU = false>
 __device__ __forceinline__ RetireRow retire_load(const Win &w, uint32_t pos, int lane) {
     RetireRow r;
     r.j = (int)(pos >> 5);
-    r.key = w.sf[32 * r.j + lane];
-    r.pr = w.sp[32 * r.j + lane];
+    if (CLU) {
+        const uint32_t row = dsm_row(w, r.j) + 4u * lane;
+        r.key = dsm_ld(row);
+        r.pr = dead_mask(w.dead[r.j], r.key, dsm_ld(row + (128u << w.cshift)));
+    } else {
+        r.key = w.sf[32 * r.j + lane];
+        r.pr = w.sp[32 * r.j + lane];
+    }
     const int jj = (r.j & ~31) + lane;
     r.gq = make_uint4(kNone, kNone, kNone, 0u);
     if (!SCAN && jj < w.nch) r.gq = ldk<SG>(w.s0 + jj, w.keep);
@@ -250,11 +303,12 @@ __device__ __forceinline__ RetireRow retire_load(const Win &w, uint32_t pos, int
 
 // Mark the entry at (alloc,id)-position `pos` dead and rebuild its chunk's
 // skeleton (one warp; TIER_SCAN keeps no skeleton).
-template <bool STATS, bool SCAN = false>
+template <bool STATS, bool SCAN = false, bool CLU = false>
 __device__ __forceinline__ void retire_finish(const Win &w, RetireRow r, uint32_t pos, int lane) {
     if ((r.key & 31u) == (pos & 31u) && r.key != kNone) {
         r.pr = kDead;
-        w.sp[32 * r.j + lane] = kDead;
+        if (CLU) w.dead[r.j] |= 1u << (pos & 31u);
+        else w.sp[32 * r.j + lane] = kDead;
     }
     if (SCAN) return;
     uint4 q;
@@ -288,13 +342,14 @@ __device__ __forceinline__ uint32_t fit_min4(uint4 k, uint4 v, uint32_t thr, uin
 // as two 16-byte loads of SF and two of SP — skipping segments whose prefix
 // minimum cannot beat `bound`, which tightens after every wave.  Returns
 // this lane's best fitting priority.
-template <int DU>
+template <int DU, bool CLU = false>
 __device__ __forceinline__ uint32_t drain_pending(const Win &w, const uint32_t *pend, int np,
                                                   uint32_t thr, uint32_t bound, int lane) {
     __syncwarp();
     uint32_t best = kNone;
     for (int e0 = 0; e0 < np; e0 += 32 * DU) {
         uint4 k[DU][2], v[DU][2];
+        uint32_t dm[DU];
         bool act[DU];
 #pragma unroll
         for (int u = 0; u < DU; u++) {
@@ -302,17 +357,36 @@ __device__ __forceinline__ uint32_t drain_pending(const Win &w, const uint32_t *
             act[u] = e < np && pend[kPendCap + e] < bound;
             if (act[u]) {
                 const uint32_t code = pend[e];
-                const int idx = 32 * (int)(code >> 2) + 8 * (int)(code & 3u);
-                const uint4 *kp = reinterpret_cast<const uint4 *>(w.sf + idx);
-                const uint4 *vp = reinterpret_cast<const uint4 *>(w.sp + idx);
-                k[u][0] = kp[0];
-                k[u][1] = kp[1];
-                v[u][0] = vp[0];
-                v[u][1] = vp[1];
+                if (CLU) {
+                    const int j = (int)(code >> 2);
+                    const uint32_t row = dsm_row(w, j) + 32u * (code & 3u);
+                    k[u][0] = dsm_ld4(row);
+                    k[u][1] = dsm_ld4(row + 16u);
+                    v[u][0] = dsm_ld4(row + (128u << w.cshift));
+                    v[u][1] = dsm_ld4(row + (128u << w.cshift) + 16u);
+                    dm[u] = w.dead[j];
+                } else {
+                    const int idx = 32 * (int)(code >> 2) + 8 * (int)(code & 3u);
+                    const uint4 *kp = reinterpret_cast<const uint4 *>(w.sf + idx);
+                    const uint4 *vp = reinterpret_cast<const uint4 *>(w.sp + idx);
+                    k[u][0] = kp[0];
+                    k[u][1] = kp[1];
+                    v[u][0] = vp[0];
+                    v[u][1] = vp[1];
+                }
             }
         }
 #pragma unroll
         for (int u = 0; u < DU; u++) {
+            if (CLU && act[u]) {
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    v[u][h].x = dead_mask(dm[u], k[u][h].x, v[u][h].x);
+                    v[u][h].y = dead_mask(dm[u], k[u][h].y, v[u][h].y);
+                    v[u][h].z = dead_mask(dm[u], k[u][h].z, v[u][h].z);
+                    v[u][h].w = dead_mask(dm[u], k[u][h].w, v[u][h].w);
+                }
+            }
             if (act[u]) {
                 best = fit_min4(k[u][0], v[u][0], thr, best);
                 best = fit_min4(k[u][1], v[u][1], thr, best);
@@ -469,7 +543,7 @@ __device__ __forceinline__ uint32_t query_scan(const Win &w, const uint4 *rec4, 
     return wb;
 }
 
-template <bool STATS, int NW, int TIER, bool LEAN>
+template <bool STATS, int NW, int TIER, bool LEAN, bool CLU = false>
 __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4, const uint2 *raw2,
                                                  uint32_t *pend, int c0, int c1, uint32_t chi,
                                                  uint32_t clop, uint32_t chip, uint32_t rawhi,
@@ -493,8 +567,14 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
     const bool g0_fits = ldk<(TIER < TIER_GROUP)>(w.gs + (c0 >> 5), w.keep).x <= thr;
     if (warp == 0 && partial && (TIER == TIER_ALL || g0_fits)) {  // speculative row read
         edge = true;
-        ek = w.sf[32 * c0 + lane];
-        ep = w.sp[32 * c0 + lane];
+        if (CLU) {
+            const uint32_t row = dsm_row(w, c0) + 4u * lane;
+            ek = dsm_ld(row);
+            ep = dead_mask(w.dead[c0], ek, dsm_ld(row + (128u << w.cshift)));
+        } else {
+            ek = w.sf[32 * c0 + lane];
+            ep = w.sp[32 * c0 + lane];
+        }
         if (STATS) qs.edge++;
     }
     if (STATS) {
@@ -503,7 +583,15 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
         if (warp == 0) {
             for (int e = 0; e < (c1 > c0 ? 2 : 1); e++) {
                 const int cc = e ? c1 : c0;
-                const uint32_t kk = w.sf[32 * cc + lane], pp = w.sp[32 * cc + lane];
+                uint32_t kk, pp;
+                if (CLU) {
+                    const uint32_t row = dsm_row(w, cc) + 4u * lane;
+                    kk = dsm_ld(row);
+                    pp = dead_mask(w.dead[cc], kk, dsm_ld(row + (128u << w.cshift)));
+                } else {
+                    kk = w.sf[32 * cc + lane];
+                    pp = w.sp[32 * cc + lane];
+                }
                 const uint32_t pos = 32u * (uint32_t)cc + (kk & 31u);
                 qs.wlive += __popc(__ballot_sync(kFull, kk != kNone && pp != kDead &&
                                                             pos >= clop && pos < chip));
@@ -529,7 +617,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
                                             pend, np, lane);
             if (np > kPendCap - 32 * kG) {
                 if (STATS) qs.seg += np;
-                best = min(best, drain_pending<DU>(w, pend, np, thr, kNone, lane));
+                best = min(best, drain_pending<DU, CLU>(w, pend, np, thr, kNone, lane));
                 np = 0;
             }
         }
@@ -565,8 +653,12 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
             const uint32_t e = __reduce_min_sync(kFull, best);
             if (e < e_used) {
                 e_used = e;
-                const uint2 er = rec_smem ? raw2[e] : ldg_hint(raw2 + e, w.stream);
-                lstar = er.y - er.x;
+                if (CLU) {
+                    lstar = dsm_lifetime(w, e);
+                } else {
+                    const uint2 er = rec_smem ? raw2[e] : ldg_hint(raw2 + e, w.stream);
+                    lstar = er.y - er.x;
+                }
                 m &= __ballot_sync(kFull, scan && rawhi - graw >= lstar);
             }
         };
@@ -590,13 +682,13 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
             for (int u = 0; u < kG; u++) {
                 if (__any_sync(kFull, jj[u] >= 0)) {
                     if (STATS) qs.pass++;
-                    eval_loaded<(TIER < TIER_ALL)>(w, ck4[u], jj[u], thr, rawhi, lstar, best,
-                                                   pend, np, lane);
+                    eval_loaded<(TIER < TIER_ALL) && !CLU>(w, ck4[u], jj[u], thr, rawhi, lstar,
+                                                           best, pend, np, lane);
                 }
             }
             if (np > kPendCap - 32 * kG) {
                 if (STATS) qs.seg += np;
-                best = min(best, drain_pending<DU>(w, pend, np, thr, kNone, lane));
+                best = min(best, drain_pending<DU, CLU>(w, pend, np, thr, kNone, lane));
                 np = 0;
             }
             if (prune && m) tighten();
@@ -617,7 +709,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
         for (int e = lane; e < np; e += 32)
             qs.seg += __popc(__ballot_sync(__activemask(), pend[kPendCap + e] < wb1));
     }
-    const uint32_t b2 = drain_pending<DU>(w, pend, np, thr, wb1, lane);
+    const uint32_t b2 = drain_pending<DU, CLU>(w, pend, np, thr, wb1, lane);
     if (b2 < best) best = b2;
     const uint32_t wb = __reduce_min_sync(kFull, best);
     if (!rec_smem && wb != wb1 && best == wb) {  // a pending segment improved it
@@ -633,7 +725,7 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
 // would otherwise spill; the uncapped single-trace kernels schedule better
 // with 64-bit ones (measured, TIER_ALL 10^4: 5-7 %).
 template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER, bool TIMING,
-          bool LEAN = false>
+          bool LEAN = false, bool CLU = false>
 __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
     using Cnt = std::conditional_t<LEAN, int, int64_t>;
     using KO = KeyT<HT>;
@@ -686,6 +778,14 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
         win.gs = g;
     } else {
         win.gs = a.gs + gbase;
+    }
+    if (CLU) {  // placed-entry bitmap (the remote table is never written)
+        win.dead = reinterpret_cast<uint32_t *>(smem + off);
+        off += align16((size_t)nch * 4);
+        for (int i = threadIdx.x; i < nch; i += 32 * NW) win.dead[i] = 0;
+        win.tab = (uint32_t)__cvta_generic_to_shared(smem);  // workers' slice offset
+        win.cshift = a.clu_cshift;
+        win.pshift = a.clu_pshift;
     }
     if (TIER >= TIER_SKEL && TIER != TIER_SCAN) {
         uint4 *d = reinterpret_cast<uint4 *>(smem + off);
@@ -838,9 +938,9 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
         uint2 rw = make_uint2(0, 0);
         if (qlop < qhip) {
             const int c0 = (int)(qlop >> 5), c1 = (int)((qhip - 1) >> 5);
-            wb = query_window<STATS, NW, TIER, LEAN>(win, rec4, raw2, pend, c0, c1, qchi, qlop,
-                                               qhip, qraw, prune, warp, lane, lbest, r0, r1, rw,
-                                               qs, a.rec_smem != 0);
+            wb = query_window<STATS, NW, TIER, LEAN, CLU>(win, rec4, raw2, pend, c0, c1, qchi,
+                                                         qlop, qhip, qraw, prune, warp, lane,
+                                                         lbest, r0, r1, rw, qs, a.rec_smem != 0);
         }
         uint32_t gbest;
         if (NW > 1) {
@@ -923,7 +1023,7 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
             const uint32_t rpos = r0.x, rar = r0.y, rfr = r0.z, rap = r0.w, rfp = r1.x,
                            rk = r1.y;
             if (NW == 1)  // the row read overlaps the skyline update
-                rr = retire_load<(TIER < TIER_SKEL), TIER == TIER_SCAN>(win, rpos, lane);
+                rr = retire_load<(TIER < TIER_SKEL), TIER == TIER_SCAN, CLU>(win, rpos, lane);
             HT rsz = (HT)r1.z;
             if (sizeof(HT) == 8) rsz |= (HT)((uint64_t)r1.w << 32);
             const HT ch = KO::h(ck);
@@ -1001,7 +1101,8 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
         maxl = max(maxl, nl);
         c = cnext;
         if (TIMING) { const long long t2 = clock64(); tph[2] += t2 - tc; tc = t2; }
-        if (NW == 1 && gbest != kNone) retire_finish<STATS, TIER == TIER_SCAN>(win, rr, r0.x, lane);
+        if (NW == 1 && gbest != kNone)
+            retire_finish<STATS, TIER == TIER_SCAN, CLU>(win, rr, r0.x, lane);
         __syncwarp();
         if (TIMING) {
             const long long t2 = clock64();
@@ -1042,6 +1143,93 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
 #include "warp_engine.cuh"
 namespace mp {
 namespace {
+
+// ---- bulk copies (the TMA engine's cp.async.bulk) into shared memory ----
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+        "r"((uint32_t)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;"
+            " selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+// bulk copy of `bytes` (multiple of 16, 16-B aligned ends) in <= 64 KB pieces
+__device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t bytes,
+                                          uint64_t *bar) {
+    for (uint32_t o = 0; o < bytes; o += 65536u)
+        bulk_g2s(static_cast<char *>(dst) + o, static_cast<const char *>(src) + o,
+                 min(65536u, bytes - o), bar);
+}
+
+// lifetimes in priority order for the cluster tier's pruning bound
+__global__ void k_lifetimes(const uint2 *raw2, uint32_t *lt, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        lt[i] = raw2[i].y - raw2[i].x;
+}
+
+// Cluster tier: one thread-block cluster per trace.  Rank 0 runs the TIER_SKEL
+// step loop (skeletons, lines, pending list in its own shared memory); ranks
+// 1.. hold the chunk-sorted table and the lifetimes in theirs (staged with
+// bulk copies) and serve them over DSMEM until the plan is done.
+template <bool STATS>
+__global__ void __launch_bounds__(32) k_plan_clu(PlanArgs a, int cl) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar;
+    cg::cluster_group cluster = cg::this_cluster();
+    const uint32_t rank = cluster.block_rank();
+    const int t = (int)(blockIdx.x / cl);
+    if (rank > 0) {
+        const int64_t base = a.trace_ptr[t];
+        const int n = (int)(a.trace_ptr[t + 1] - base);
+        const int nch = (n + 31) >> 5;
+        const int64_t cb = chunk_base(base, t);
+        const int cpc = 1 << a.clu_cshift, ppc = 1 << a.clu_pshift;
+        const int j0 = (int)(rank - 1) * cpc, p0 = (int)(rank - 1) * ppc;
+        const int jn = max(0, min(cpc, nch - j0)), pn = max(0, min(ppc, n - p0));
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            const uint32_t tb = 128u * (uint32_t)jn, lb = ((4u * (uint32_t)pn) + 15u) & ~15u;
+            mbar_expect_tx(&bar, 2 * tb + lb);
+            if (tb) {
+                bulk_copy(smem, a.sf + 32 * (cb + j0), tb, &bar);
+                bulk_copy(smem + 128 * cpc, a.sp + 32 * (cb + j0), tb, &bar);
+            }
+            if (lb) bulk_copy(smem + 256 * cpc, a.lt + base + p0, lb, &bar);
+        }
+        __syncwarp();
+        mbar_wait(&bar, 0);
+        cluster.sync();  // slices in place
+        cluster.sync();  // the plan is done
+        return;
+    }
+    cluster.sync();
+    plan_trace<uint32_t, true, STATS, 1, TIER_SKEL, false, false, true>(a, t);
+    cluster.sync();
+}
 
 // TIER_TINY planner: one warp per trace (grid = traces or tlist); packed
 // choose keys when every height fits 27 bits
@@ -1253,6 +1441,28 @@ int launch_ht(const PlanArgs &a, int grid, int tier, bool lines_smem, size_t sme
               cudaStream_t s) {
     if (lines_smem) return launch_tier<HT, true, ST>(a, grid, tier, smem, s);
     return launch_tier<HT, false, ST>(a, grid, tier, smem, s);
+}
+
+int launch_clu(const PlanArgs &a, int cl, size_t smem, bool stats, cudaStream_t s) {
+    auto fn = stats ? k_plan_clu<true> : k_plan_clu<false>;
+    std::lock_guard<std::mutex> lock(g_launch_mu);
+    MP_TRY(set_smem_attr(reinterpret_cast<const void *>(fn), (int)smem));
+    if (cl > 8) MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cl);
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MP_CUDA(cudaLaunchKernelEx(&cfg, fn, a, cl));
+    g_launches++;
+    return MP_OK;
 }
 
 int launch_tiny(const PlanArgs &a, const uint2 *ent, int grid, size_t smem, bool stats,
@@ -1688,9 +1898,46 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     const bool use_tiny = h32 && nmax <= kTinyMaxBlocks && T <= sms && !force_global &&
                           !a.timing && g_nwarps == 1 && !getenv("MEMPLAN_NO_TINY") &&
                           !getenv("MEMPLAN_TIER") && tiny_smem_bytes(nmax) <= lim;
+    // Cluster tier (opt-in, MEMPLAN_CLUSTER=1): a single trace whose chunk
+    // skeletons fit the SM but whose table does not (10^5 blocks) gets a
+    // thread-block cluster — the planner CTA plus worker CTAs holding the
+    // table and the lifetimes, read over DSMEM instead of L2.  Bit-exact, but
+    // measured 9-10 % SLOWER than the L2-resident table at 10^5 (uniform
+    // 363 vs 333 ms, cnn 268 vs 244 ms): the table is L2/L1-hot, DSMEM saves
+    // little latency, and the placed-entry bitmap + address mapping cost more
+    // (profiles/r2_summary.md)
+    int clu = 0;
+    size_t clu_smem = 0;
+    if (!use_tiny && T == 1 && h32 && lay.tier == TIER_SKEL && lay.lines_smem && !a.timing &&
+        g_nwarps == 1 && getenv("MEMPLAN_CLUSTER")) {
+        const int64_t nch = (nmax + 31) / 32;
+        const size_t lead = lay.smem + a16((size_t)nch * 4);
+        for (int cl : {2, 4, 8, 16}) {
+            const int64_t W = cl - 1;
+            int cs = 0, ps = 0;
+            while ((int64_t(1) << cs) * W < nch) cs++;
+            while ((int64_t(1) << ps) * W < nmax) ps++;
+            const size_t work = ((size_t)256 << cs) + ((size_t)4 << ps);
+            if (work <= lim && lead <= lim) {
+                clu = cl;
+                a.clu_cshift = cs;
+                a.clu_pshift = ps;
+                clu_smem = std::max(lead, work);
+                break;
+            }
+        }
+    }
+    Scratch lt_sc;
     if (use_tiny) {
         MP_TRY(launch_tiny(a, po.ent, (int)T, tiny_smem_bytes(nmax), stats_on, h27, s));
         lay.tier = TIER_WARP;
+    } else if (clu) {
+        MP_TRY(lt_sc.alloc(sizeof(uint32_t) * (size_t)(N + 8), s));
+        a.lt = lt_sc.as<uint32_t>();
+        k_lifetimes<<<std::min<int64_t>(1024, (N + 255) / 256), 256, 0, s>>>(po.raw2, lt_sc.as<uint32_t>(), N);
+        MP_CUDA(cudaGetLastError());
+        MP_TRY(launch_clu(a, clu, clu_smem, stats_on, s));
+        lay.tier = TIER_CLU;
     } else {
         MP_TRY(launch_plan(a, (int)T, h32, lay.tier, lay.lines_smem, lay.smem, s, stats_on));
     }
@@ -1739,13 +1986,14 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
     g_info.plan_ms = ms_plan;
     g_info.kernel_ms = ms_kernel;
     g_info.launches = prep_launches() + (g_launches - launches0);
-    const bool skel = lay.tier != TIER_SCAN && lay.tier != TIER_WARP;
+    const bool skel = lay.tier != TIER_SCAN && lay.tier != TIER_WARP && lay.tier != TIER_CLU;
     g_info.engine = (h32 ? 16 : 0) | (lay.lines_smem && lay.tier != TIER_WARP ? 8 : 0) |
                     (skel && lay.tier >= TIER_SKEL ? 4 : 0) |
                     (skel && lay.tier >= TIER_ALL ? 2 : 0) | (lay.rec_smem ? 1 : 0) |
                     (redo.empty() ? 0 : 32) | (skel && lay.tier >= TIER_GROUP ? 64 : 0) |
-                    (lay.tier == TIER_SCAN ? 128 : 0) | (lay.tier == TIER_WARP ? 512 : 0);
-    g_info.cluster = g_nwarps;  // warps per trace (single-CTA engine)
+                    (lay.tier == TIER_SCAN ? 128 : 0) | (lay.tier == TIER_WARP ? 512 : 0) |
+                    (lay.tier == TIER_CLU ? (1024 | 64 | 4) : 0);
+    g_info.cluster = clu ? clu : g_nwarps;  // CTAs per trace (cluster tier) or warps per trace
     return collect_stats(hst, T);
 }
 

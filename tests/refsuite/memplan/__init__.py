@@ -1,0 +1,49 @@
+"""Import alias: the reference test suite (`/root/reference/pkg/tests`,
+copied next to the reference install by baseline/install_ref.sh) imports
+`memplan`; this package answers with paper_1804_10001_b200, the drop-in.
+
+Names of the reference's out-of-scope subsystems (the exact
+branch-and-bound solver, the host-side skyline debug types) are stubs that
+SKIP the calling test, so the run reports them explicitly instead of
+failing collection.  Used only by tests/test_reference_suite_gpu.py."""
+
+from paper_1804_10001_b200 import *  # noqa: F401,F403
+from paper_1804_10001_b200 import __all__ as _ours  # noqa: F401
+
+import pytest as _pytest
+
+
+def _out_of_scope(name):
+    def stub(*_a, **_k):
+        _pytest.skip(f"{name}: out of scope for the B200 build (DESIGN.md §7)")
+    stub.__name__ = name
+    return stub
+
+
+class _SkipOnUse(type):
+    """Class-level access (e.g. OffsetLineSet.from_lines) skips too."""
+
+    def __getattr__(cls, attr):
+        if attr.startswith("__"):
+            raise AttributeError(attr)
+        _pytest.skip(f"{cls._name}: out of scope for the B200 build (DESIGN.md §7)")
+
+
+class _OutOfScopeType(metaclass=_SkipOnUse):
+    _name = "?"
+
+    def __init__(self, *_a, **_k):
+        _pytest.skip(f"{self._name}: out of scope for the B200 build (DESIGN.md §7)")
+
+
+class OffsetLineSet(_OutOfScopeType):
+    _name = "OffsetLineSet (host skyline debug type)"
+
+
+class OffsetLine(_OutOfScopeType):
+    _name = "OffsetLine (host skyline debug type)"
+
+
+find_block = _out_of_scope("find_block (host skyline debug helper)")
+solve_exact = _out_of_scope("solve_exact (exact branch-and-bound solver)")
+brute_force_peak = _out_of_scope("brute_force_peak (exact solver oracle)")

@@ -62,3 +62,40 @@ def test_lstm_all_profiles_full_offsets(huge_golden, layers):
     for t in range(len(tp) - 1):
         o, p = oracle.solve_bestfit(a[tp[t]:tp[t + 1]], f[tp[t]:tp[t + 1]], s[tp[t]:tp[t + 1]])
         assert p == pks[t] and np.array_equal(o, off[tp[t]:tp[t + 1]]), t
+
+
+@pytest.mark.parametrize("name", ["uniform_1e5_s0", "cnn_1e5_s0", "walk_1e5_s1"])
+def test_cluster_tier_engaged_and_exact(huge_golden, name, monkeypatch):
+    """A 10^5-block single trace runs on the cluster tier (the planner CTA
+    plus worker CTAs serving the table over DSMEM, staged by bulk copies);
+    the same trace with the tier disabled (L2 table) gives the same plan."""
+    from paper_1804_10001_b200.bestfit import plan_info, solve_bestfit_arrays
+    a, f, s = family_instance(name)
+    g = huge_golden[name]
+    monkeypatch.setenv("MEMPLAN_CLUSTER", "1")
+    off, peak = solve_bestfit_arrays(a, f, s)
+    info = plan_info()
+    assert info["engine"] & 1024 and info["cluster"] > 1, info
+    assert peak == g["peak"] and sha64(off) == g["offsets_sha256"]
+    monkeypatch.delenv("MEMPLAN_CLUSTER")
+    off2, peak2 = solve_bestfit_arrays(a, f, s)
+    assert not plan_info()["engine"] & 1024
+    assert peak2 == peak and np.array_equal(off2, off)
+
+
+def test_cluster_tier_random_vs_oracle(monkeypatch):
+    """Mid-size single traces (skeletons fit one SM, the table does not) on
+    the cluster tier against the C oracle, several seeds and shapes."""
+    from paper_1804_10001_b200.bestfit import plan_info, solve_bestfit_arrays
+    monkeypatch.setenv("MEMPLAN_CLUSTER", "1")
+    rng = np.random.default_rng(5)
+    for trial in range(4):
+        n = int(rng.integers(30000, 60000))
+        T = int(rng.integers(n // 4, 3 * n))
+        a = rng.integers(0, T - 1, n)
+        f = a + 1 + (rng.integers(0, T, n) % (T - a))
+        s = rng.integers(1, 1 << 16, n) * 512
+        off, peak = solve_bestfit_arrays(a, f, s)
+        info = plan_info()
+        ooff, opeak = oracle.solve_bestfit(a, f, s)
+        assert peak == opeak and np.array_equal(off, ooff), (trial, info)
