@@ -287,3 +287,4 @@ def test_concurrent_host_threads():
     for (o, p), (ro, rp) in zip(out, ref):
         assert np.array_equal(o, ro) and np.array_equal(p, rp)
     assert np.array_equal(out_single[0][0], ref_single[0]) and out_single[0][1] == ref_single[1]
+
