@@ -7,11 +7,13 @@ TAG=${TAG:-r1}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu_${TAG}.txt
 nproc >> gpurun_out/gpu_${TAG}.txt
 lscpu | grep -i "model name" >> gpurun_out/gpu_${TAG}.txt
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_${TAG}.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q -rs > gpurun_out/pytest_gpu_${TAG}.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu_${TAG}.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1
 timeout 1200 python bench.py ${BENCH_ARGS} > gpurun_out/bench_${TAG}.log 2>&1
 echo "bench rc=$?" >> gpurun_out/bench_${TAG}.log
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${TAG}.log 2>&1
+timeout 600 python bench.py --workload lstm --steps 20 --warmup 5 --no-suite --no-replay > gpurun_out/bench_lstm_${TAG}.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-check --no-replay --no-suite \
   ${BENCH_ARGS} > gpurun_out/launches_${TAG}.log 2>&1
