@@ -1,4 +1,5 @@
 // extern "C" planning entry points (include/memplan_b200.h).
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -30,6 +31,58 @@ int64_t *pinned_stage(int device) {
 
 int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *alloc,
                const int64_t *free_, const int64_t *size, int64_t T, int64_t *offsets_out,
+               int64_t *peaks_out, int flags, int device, cudaStream_t s);
+
+// Largest batch one K0 pass plans: its ranks are 32-bit over the batch's 2N
+// times (N < 2^30), and the device must hold the inputs, outputs and
+// ~110 B/block of tables (MEMPLAN_MAX_BATCH_BLOCKS overrides, for tests).
+int64_t batch_block_limit(bool host_inputs) {
+    if (const char *env = getenv("MEMPLAN_MAX_BATCH_BLOCKS")) return std::max<int64_t>(1, atoll(env));
+    size_t free_b = 0, total_b = 0;
+    int64_t lim = int64_t(1) << 29;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+        lim = std::min<int64_t>(lim, (int64_t)(free_b / (host_inputs ? 160 : 128)));
+    cudaGetLastError();
+    return std::max<int64_t>(lim, int64_t(1) << 20);
+}
+
+// A batch above the limit is planned as consecutive trace ranges, each one
+// ordinary plan (traces are independent, so the results are the same); the
+// plan info reports the sum.
+int plan_chunked(const std::vector<int64_t> &tp_h, const int64_t *alloc, const int64_t *free_,
+                 const int64_t *size, int64_t T, int64_t *offsets_out, int64_t *peaks_out,
+                 int flags, int device, cudaStream_t s, int64_t lim) {
+    mp_plan_info sum{};
+    int64_t t0 = 0;
+    while (t0 < T) {
+        int64_t t1 = t0 + 1;
+        while (t1 < T && tp_h[t1 + 1] - tp_h[t0] <= lim) t1++;
+        const int64_t b0 = tp_h[t0];
+        std::vector<int64_t> tp((size_t)(t1 - t0 + 1));
+        for (int64_t i = 0; i <= t1 - t0; i++) tp[i] = tp_h[t0 + i] - b0;
+        MP_TRY(plan_entry(tp.data(), false, alloc + b0, free_ + b0, size + b0, t1 - t0,
+                          offsets_out + b0, peaks_out + t0, flags, device, s));
+        const mp_plan_info &o = last_plan_info();
+        sum.steps += o.steps;
+        sum.lifts += o.lifts;
+        sum.max_lines = std::max(sum.max_lines, o.max_lines);
+        sum.prep_ms += o.prep_ms;
+        sum.plan_ms += o.plan_ms;
+        sum.kernel_ms += o.kernel_ms;
+        sum.engine |= o.engine;
+        sum.cluster = std::max(sum.cluster, o.cluster);
+        sum.sum_wlive += o.sum_wlive;
+        sum.launches += o.launches;
+        for (int k = 0; k < 4; k++) sum.diag[k] += o.diag[k];
+        for (int k = 0; k < 6; k++) sum.cycles[k] += o.cycles[k];
+        t0 = t1;
+    }
+    set_plan_info(sum);
+    return MP_OK;
+}
+
+int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *alloc,
+               const int64_t *free_, const int64_t *size, int64_t T, int64_t *offsets_out,
                int64_t *peaks_out, int flags, int device, cudaStream_t s) {
     MP_TRY(use_device(device));
     if (T < 0) {
@@ -51,6 +104,12 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
         }
     }
     const int64_t N = T ? tp_h[T] : 0;
+    if (T > 1 && (N > (int64_t(1) << 20) || getenv("MEMPLAN_MAX_BATCH_BLOCKS"))) {
+        const int64_t lim = batch_block_limit(!(flags & MP_DEVICE_PTRS));
+        if (N > lim)
+            return plan_chunked(tp_h, alloc, free_, size, T, offsets_out, peaks_out, flags, device,
+                                s, lim);
+    }
     if (flags & MP_DEVICE_PTRS) {
         const int64_t *tp_d = trace_ptr;
         Scratch tps;

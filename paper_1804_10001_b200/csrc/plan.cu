@@ -1565,6 +1565,7 @@ Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwar
 }  // namespace
 
 const mp_plan_info &last_plan_info() { return g_info; }
+void set_plan_info(const mp_plan_info &info) { g_info = info; }
 
 void *plan_workspace(size_t bytes, cudaStream_t s) {
     // one per thread and device; grown (never shrunk) on demand

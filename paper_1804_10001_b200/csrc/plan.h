@@ -29,5 +29,7 @@ int plan_device(const int64_t *trace_ptr_d, const int64_t *trace_ptr_h, int64_t 
 void *plan_workspace(size_t bytes, cudaStream_t s);
 
 const mp_plan_info &last_plan_info();
+// Replace this thread's plan info (chunked batches report their sum).
+void set_plan_info(const mp_plan_info &info);
 
 }  // namespace mp

@@ -288,3 +288,23 @@ def test_concurrent_host_threads():
         assert np.array_equal(o, ro) and np.array_equal(p, rp)
     assert np.array_equal(out_single[0][0], ref_single[0]) and out_single[0][1] == ref_single[1]
 
+
+
+def test_batches_beyond_one_pass_are_chunked(small_plans, monkeypatch):
+    """A batch above the per-pass block limit (32-bit K0 ranks, device
+    memory) is planned as consecutive trace ranges inside the library; the
+    results equal one pass (limit lowered with MEMPLAN_MAX_BATCH_BLOCKS)."""
+    from paper_1804_10001_b200.bestfit import plan_info, solve_bestfit_batched_arrays
+    cases = small_plans
+    tp = np.zeros(len(cases) + 1, np.int64)
+    np.cumsum([len(c["blocks"]) for c in cases], out=tp[1:])
+    cols = [blocks_arrays(c["blocks"]) for c in cases]
+    a, f, s = (np.concatenate([c[i] for c in cols]) for i in range(3))
+    one_off, one_pk = solve_bestfit_batched_arrays(tp, a, f, s)
+    launches_one = plan_info()["launches"]
+    monkeypatch.setenv("MEMPLAN_MAX_BATCH_BLOCKS", "3000")
+    off, pk = solve_bestfit_batched_arrays(tp, a, f, s)
+    assert plan_info()["launches"] > launches_one
+    assert np.array_equal(off, one_off) and np.array_equal(pk, one_pk)
+    for t, c in enumerate(cases):
+        assert pk[t] == c["peak"] and off[tp[t]:tp[t + 1]].tolist() == c["offsets"], c["name"]
