@@ -1,5 +1,7 @@
 # compute-sanitizer memcheck / racecheck / synccheck on the planner, validator
-# and prep kernels over small traces (single and batched).
+# and prep kernels over small traces (single and batched): TIER_TINY (single
+# and fused, incl. the staircase restart), the LEAN batched kernel, and the
+# cluster tier (DSMEM table, bulk-copy fills).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 cat > /tmp/san_case.py <<'PY'
@@ -31,7 +33,16 @@ for sizes in ([13] * 300, [400] * 200):
 # register-capped LEAN batched kernel + composite / raw-rank K0 (N >= 2^16)
 tp, cat = batch([2100] * 160, 11)
 solve_bestfit_batched_arrays(tp, *cat)
-print("case ok", pk)
+# cluster tier (opt-in): planner CTA + worker CTAs, table over DSMEM, bulk-copy fills
+os.environ["MEMPLAN_CLUSTER"] = "1"
+a2, f2, s2 = uniform_arrays(40000, 3); s2 = ((s2 + 511) // 512) * 512
+from paper_1804_10001_b200.bestfit import plan_info
+off2, pk2 = solve_bestfit_arrays(a2, f2, s2)
+assert plan_info()["engine"] & 1024, plan_info()
+del os.environ["MEMPLAN_CLUSTER"]
+off3, pk3 = solve_bestfit_arrays(a2, f2, s2)
+assert pk2 == pk3 and (off2 == off3).all()
+print("case ok", pk, pk2)
 PY
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 3 python /tmp/san_case.py > gpurun_out/san_$tool.log 2>&1
