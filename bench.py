@@ -747,7 +747,11 @@ def roofline(args, T: int, NB: int, info_stats: dict, kms: float, lat_ms, single
     steps_total = float(info_stats["steps"])
     achieved = steps_total / (kms / 1e3)
     resident = max(1, min(16, -(-T // N_SMS)))
-    fl_batch = step_floor(0, N_SMS * resident)
+    # the window table is in shared memory for TIER_TINY / TIER_SCAN / TIER_ALL
+    # (engine bits 512 / 128 / 2): the floor's table read is an LDS there
+    eng = int(info_stats.get("engine", 0))
+    smem_table = bool(eng & (512 | 128 | 2))
+    fl_batch = step_floor(1 if smem_table else 0, N_SMS * resident)
     fl_one = step_floor(0, 1)
     fl_one_smem = step_floor(1, 1)
     peak = fl_batch["steps_per_s"] if fl_batch else None
@@ -763,11 +767,13 @@ def roofline(args, T: int, NB: int, info_stats: dict, kms: float, lat_ms, single
     out = {
         "bound": "latency", "unit": "trace-steps/s", "achieved": achieved, "peak": peak,
         "frac": (achieved / peak) if peak else None, "traffic": traffic,
-        "kernel": "k_plan_occ (K2 batched planner)", "kernel_ms": kms,
+        "kernel": ("k_plan_occ (K2 batched planner)" if resident > 1 else
+                   "planner (K1/K2, engine %d)" % eng), "kernel_ms": kms,
         "steps_per_launch": steps_total, "steps_per_trace": steps_total / max(T, 1),
         "traces_resident_per_sm": resident,
         "peak_def": (f"measured step rate of the minimal dependent step (LDS argmin + REDUX + "
-                     f"VOTE/SHFL, one dependent L2 table read + REDUX, STS update) with "
+                     f"VOTE/SHFL, one dependent {'shared-memory' if smem_table else 'L2'} "
+                     f"table read + REDUX, STS update) with "
                      f"{resident} one-warp traces per SM on {N_SMS} SMs "
                      f"(tools/ubench/step_floor.cu)"),
         "floor_batch": fl_batch,
