@@ -134,13 +134,10 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
     Scratch buf;
     int64_t *tp_d;
     if (stage) {
-        static thread_local Scratch io[64];
-        Scratch &w = io[device];
-        if (w.bytes < in_b + out_b + 256 || w.stream != s) {
-            if (w.ptr) cudaStreamSynchronize(w.stream);
-            MP_TRY(w.alloc(std::max(in_b + out_b + 256, w.bytes + w.bytes / 2), s));
-        }
-        tp_d = w.as<int64_t>();
+        static thread_local KeptBuffer io[64];
+        void *p = io[device].get(in_b + out_b + 256);
+        if (!p) return cuda_fail(cudaGetLastError(), "cudaMalloc(plan staging)");
+        tp_d = static_cast<int64_t *>(p);
     } else {
         MP_TRY(buf.alloc(in_b + out_b + 256, s));
         tp_d = buf.as<int64_t>();

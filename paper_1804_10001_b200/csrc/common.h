@@ -50,6 +50,38 @@ struct Scratch {
     template <typename T> T *as() const { return static_cast<T *>(ptr); }
 };
 
+// Device buffer kept for a thread's lifetime and grown on demand (plain
+// cudaMalloc, not stream-ordered: every user synchronises its stream before
+// the buffer is reused, and the destructor does not depend on a stream the
+// caller may already have destroyed).
+struct KeptBuffer {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    KeptBuffer() = default;
+    KeptBuffer(const KeptBuffer &) = delete;
+    KeptBuffer &operator=(const KeptBuffer &) = delete;
+    ~KeptBuffer() {
+        if (ptr) cudaFree(ptr);
+    }
+    // nullptr on failure (the CUDA error is left for the caller's check)
+    void *get(size_t n) {
+        if (n <= bytes && ptr) return ptr;
+        const size_t want = n > bytes + bytes / 2 ? n : bytes + bytes / 2;
+        if (ptr) {
+            cudaDeviceSynchronize();  // no kernel of another stream still reads it
+            cudaFree(ptr);
+            ptr = nullptr;
+            bytes = 0;
+        }
+        if (cudaMalloc(&ptr, want) != cudaSuccess) {
+            ptr = nullptr;
+            return nullptr;
+        }
+        bytes = want;
+        return ptr;
+    }
+};
+
 // Bump sub-allocator over one Scratch (keeps the number of pool calls at one
 // per plan).  All carve-outs are 256-byte aligned.
 struct Carver {

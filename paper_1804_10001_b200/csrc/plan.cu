@@ -1569,16 +1569,12 @@ void set_plan_info(const mp_plan_info &info) { g_info = info; }
 
 void *plan_workspace(size_t bytes, cudaStream_t s) {
     // one per thread and device; grown (never shrunk) on demand
-    static thread_local Scratch ws[64];
+    (void)s;
+    static thread_local KeptBuffer ws[64];
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return nullptr;
-    Scratch &w = ws[dev];
-    if (w.bytes < bytes || w.stream != s) {
-        if (w.ptr) cudaStreamSynchronize(w.stream);  // no plan still reads it
-        if (w.alloc(std::max(bytes, w.bytes + w.bytes / 2), s) != MP_OK) return nullptr;
-    }
-    return w.ptr;
+    return ws[dev].get(bytes);
 }
 
 namespace {
