@@ -139,7 +139,7 @@ class Clocks:
         self.proc = None
 
     def start(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+        q = self.q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
@@ -161,6 +161,15 @@ class Clocks:
         self.proc.terminate()
         self.proc.wait()
         self.thread.join(timeout=2)
+        if not self.rows:  # a timed region shorter than one sampling period
+            try:
+                r = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.q}",
+                                    "--format=csv,noheader,nounits"], capture_output=True,
+                                   text=True, timeout=30)
+                self.rows = [[x.strip() for x in line.split(",")]
+                             for line in r.stdout.splitlines() if line.strip()]
+            except (OSError, subprocess.SubprocessError):
+                pass
         sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]

@@ -1707,15 +1707,23 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
                           : launch_fused<256, 16>(a, in, (int)T, smem, stats_on, tiny, s);
     if (rc != MP_OK) return rc;
     cudaEventRecord(k1, s);
-    k_reduce_stats<<<1, kRedThreads, 0, s>>>(stats, T, red);
-    MP_CUDA(cudaGetLastError());
-    g_launches++;
+    // one trace: its stats row is the reduction (no extra launch)
+    if (T > 1) {
+        k_reduce_stats<<<1, kRedThreads, 0, s>>>(stats, T, red);
+        MP_CUDA(cudaGetLastError());
+        g_launches++;
+    }
     // host-array callers: their results ride the same round trip
     if (hc) MP_CUDA(cudaMemcpyAsync(hc->dst, hc->src, hc->bytes, cudaMemcpyDeviceToHost, s));
-    MP_CUDA(cudaMemcpyAsync(g_fctx.red_h, red, sizeof(int64_t) * (ST_N + 2),
-                            cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(g_fctx.red_h, T > 1 ? red : stats,
+                            sizeof(int64_t) * (T > 1 ? ST_N + 2 : ST_N), cudaMemcpyDeviceToHost,
+                            s));
     MP_CUDA(cudaStreamSynchronize(s));
     std::vector<int64_t> hst(g_fctx.red_h, g_fctx.red_h + ST_N + 2);
+    if (T == 1) {  // the reduction's extra slots: overflowed traces, first failing trace
+        hst[ST_N] = hst[ST_STATUS] == PS_LINES_OVERFLOW ? 1 : 0;
+        hst[ST_N + 1] = hst[ST_STATUS] != PS_OK && hst[ST_STATUS] != PS_LINES_OVERFLOW ? 0 : 1;
+    }
     float ms = 0;
     cudaEventElapsedTime(&ms, k0, k1);
     if (hst[ST_N] > 0) return kFusedFallback;

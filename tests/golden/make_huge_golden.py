@@ -108,7 +108,7 @@ def run(job: str) -> dict:
 
 JOBS = ["lstm_L6", "lstm_L64", "lstm_L6_a512", "lstm_L64_a512",
         "uniform_1e5_s0", "cnn_1e5_s0", "walk_1e5_s0", "uniform_1e5_s1", "walk_1e5_s1",
-        "cnn_1e6_s0", "uniform_1e6_s0"]
+        "cnn_1e6_s0", "uniform_1e6_s0", "walk_1e6_s0"]
 
 
 def main() -> None:
