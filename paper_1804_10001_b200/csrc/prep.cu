@@ -8,6 +8,7 @@
 // Batched form: T traces in CSR (trace_ptr).  Every sort is a stable CUB
 // radix sort; the per-trace grouping is restored by a final stable sort on
 // the trace index (LSD order), so a single pass handles one or many traces.
+#include <cub/block/block_scan.cuh>
 #include <cub/cub.cuh>
 
 #include <stdlib.h>
@@ -169,6 +170,45 @@ __global__ void k_sorted_arank(const uint32_t *__restrict__ order, const uint32_
         sar[p] = arank[order[p]];
 }
 
+// LOP table per trace: lop[off_t + r] = first (alloc, id)-position whose
+// alloc rank is >= r, for r in [0, U_t] — built by one pass over the sorted
+// alloc ranks (each position writes the ranks since its predecessor's), so
+// k_pack reads apos/fpos with one load each instead of two binary searches.
+// off_t = sum over earlier traces of (U + 1): one block scans the T values.
+__global__ void __launch_bounds__(1024) k_lop_offsets(const uint32_t *__restrict__ U, int64_t T,
+                                                      uint64_t *__restrict__ off) {
+    using BS = cub::BlockScan<uint64_t, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    const int64_t per = (T + 1023) / 1024;
+    const int64_t lo = threadIdx.x * per, hi = T < lo + per ? T : lo + per;
+    uint64_t sum = 0;
+    for (int64_t t = lo; t < hi; t++) sum += (uint64_t)U[t] + 1u;
+    uint64_t pre = 0, total = 0;
+    BS(tmp).ExclusiveSum(sum, pre, total);
+    for (int64_t t = lo; t < hi; t++) {
+        off[t] = pre;
+        pre += (uint64_t)U[t] + 1u;
+    }
+    if (threadIdx.x == 0) off[T] = total;
+}
+
+__global__ void k_lop_fill(const uint32_t *__restrict__ tix, const int64_t *__restrict__ trace_ptr,
+                           const uint32_t *__restrict__ sar, const uint32_t *__restrict__ U,
+                           const uint64_t *__restrict__ off, int64_t N, uint32_t *__restrict__ lop) {
+    for (int64_t P = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; P < N;
+         P += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = tix[P];
+        const int64_t b = trace_ptr[t];
+        const uint32_t p = (uint32_t)(P - b), n = (uint32_t)(trace_ptr[t + 1] - b);
+        uint32_t *L = lop + off[t];
+        const uint32_t cur = sar[P];
+        const uint32_t first = p ? sar[P - 1] + 1u : 0u;  // ranks (prev, cur]
+        for (uint32_t r = first; r <= cur; r++) L[r] = p;
+        if (p + 1 == n)
+            for (uint32_t r = cur + 1; r <= U[t]; r++) L[r] = n;
+    }
+}
+
 __device__ __forceinline__ int64_t gcd64(int64_t a, int64_t b) {
     while (b) {
         int64_t t = a % b;
@@ -261,7 +301,8 @@ __global__ void k_pack(const uint32_t *__restrict__ tix, const int64_t *__restri
                        const int64_t *__restrict__ unit, const int64_t *__restrict__ alloc,
                        const int64_t *__restrict__ free_, const int64_t *__restrict__ tmin,
                        int64_t N, uint2 *__restrict__ ent, Rec *__restrict__ rec,
-                       uint2 *__restrict__ raw2, uint32_t *__restrict__ rawpos) {
+                       uint2 *__restrict__ raw2, uint32_t *__restrict__ rawpos,
+                       const uint32_t *__restrict__ lop, const uint64_t *__restrict__ off) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
          k += (int64_t)gridDim.x * blockDim.x) {
         uint32_t t = tix[k];
@@ -272,8 +313,14 @@ __global__ void k_pack(const uint32_t *__restrict__ tix, const int64_t *__restri
         r.pos = posof[k];
         r.arank = arank[k];
         r.frank = frank[k];
-        r.apos = lower_bound_u32(s, n, r.arank);
-        r.fpos = lower_bound_u32(s, n, r.frank);
+        if (lop) {  // LOP table (k_lop_fill)
+            const uint32_t *L = lop + off[t];
+            r.apos = L[r.arank];
+            r.fpos = L[r.frank];
+        } else {
+            r.apos = lower_bound_u32(s, n, r.arank);
+            r.fpos = lower_bound_u32(s, n, r.frank);
+        }
         r.k = (uint32_t)(k - b);
         r.size = size[k] / unit[t];  // in units of the trace's size gcd
         rec[b + prio[k]] = r;
@@ -687,9 +734,28 @@ int prep_run(const PrepIn &in, PrepOut &out, void *scratch, size_t scratch_bytes
                                                       out.tspan);
         g_prep_k++;
     }
+    // LOP table in the dead time-sort buffers (times + times_s: 8N words)
+    // when the ranks span at most ~4 per block (dense ranks: U <= 2n; raw
+    // ranks: U = time span + 1) — else the binary searches
+    uint32_t *lop = nullptr;
+    const uint64_t *loff = nullptr;
+    if (T + 1 <= N && !getenv("MEMPLAN_NO_LOP")) {
+        uint64_t *offd = k64_s;
+        k_lop_offsets<<<1, 1024, 0, s>>>(out.U, T, offd);
+        g_prep_k++;
+        uint64_t total = 0;
+        MP_CUDA(cudaMemcpyAsync(&total, offd + T, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        if (total <= (uint64_t)(8 * N)) {
+            lop = reinterpret_cast<uint32_t *>(times);  // times_s follows contiguously
+            loff = offd;
+            k_lop_fill<<<g1, kThreads, 0, s>>>(tix, in.trace_ptr, sar, out.U, offd, N, lop);
+            g_prep_k++;
+        }
+    }
     k_pack<<<g1, kThreads, 0, s>>>(tix, in.trace_ptr, arank, frank, posof, prio, sar, in.size,
                                    out.unit, in.alloc, in.free_, out.tmin, N, out.ent, out.rec,
-                                   out.raw2, out.rawpos);
+                                   out.raw2, out.rawpos, lop, loff);
     g_prep_k++;
     if (out.sf) {
         const int64_t chunks = out.nchunks;
