@@ -144,9 +144,27 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
     }
     int64_t *a_d = tp_d + (T + 1), *f_d = a_d + N, *s_d = f_d + N;
     int64_t *o_d = s_d + N, *p_d = o_d + N;
-    // small plans (per-network planning) go through a pinned staging buffer:
-    // two copies instead of six pageable ones
-    if (stage) {
+    // small plans whose caller arrays are already page-locked (torch
+    // pin_memory, cudaHostAlloc) copy straight from and to them; otherwise
+    // (per-network planning from numpy arrays) through a pinned staging
+    // buffer: two copies instead of six pageable ones
+    auto pinned = [](const void *p) {
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return at.type == cudaMemoryTypeHost;
+    };
+    const bool direct = stage && N > 0 && T > 0 && pinned(alloc) && pinned(free_) &&
+                        pinned(size) && pinned(offsets_out) && pinned(peaks_out);
+    if (direct) {
+        memcpy(stage, tp_h.data(), sizeof(int64_t) * (T + 1));
+        MP_CUDA(cudaMemcpyAsync(tp_d, stage, sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaMemcpyAsync(a_d, alloc, nb, cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaMemcpyAsync(f_d, free_, nb, cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaMemcpyAsync(s_d, size, nb, cudaMemcpyHostToDevice, s));
+    } else if (stage) {
         memcpy(stage, tp_h.data(), sizeof(int64_t) * (T + 1));
         if (N) {
             memcpy(stage + (T + 1), alloc, nb);
@@ -164,7 +182,16 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
         }
     }
     // staged plans: the results' copy rides the planner's own synchronisation
-    HostCopy hc{stage, o_d, out_b, false};
+    HostCopy hc{{stage, nullptr}, {o_d, nullptr}, {out_b, 0}, 1, false};
+    if (direct) {
+        hc.dst[0] = offsets_out;
+        hc.src[0] = o_d;
+        hc.bytes[0] = nb;
+        hc.dst[1] = peaks_out;
+        hc.src[1] = p_d;
+        hc.bytes[1] = sizeof(int64_t) * (size_t)T;
+        hc.n = 2;
+    }
     {
         const int rc = plan_device(tp_d, tp_h.data(), T, a_d, f_d, s_d, o_d, p_d, flags, device, s,
                                    stage ? &hc : nullptr);
@@ -175,6 +202,14 @@ int plan_entry(const int64_t *trace_ptr, bool trace_ptr_is_dev, const int64_t *a
             cudaGetLastError();
             return rc;
         }
+    }
+    if (direct) {
+        if (!hc.done) {
+            MP_CUDA(cudaMemcpyAsync(offsets_out, o_d, nb, cudaMemcpyDeviceToHost, s));
+            MP_CUDA(cudaMemcpyAsync(peaks_out, p_d, sizeof(int64_t) * T, cudaMemcpyDeviceToHost, s));
+            MP_CUDA(cudaStreamSynchronize(s));
+        }
+        return MP_OK;
     }
     if (stage) {
         // the staging buffer's input part was consumed by the upload above

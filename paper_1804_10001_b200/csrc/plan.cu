@@ -1714,7 +1714,11 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
         g_launches++;
     }
     // host-array callers: their results ride the same round trip
-    if (hc) MP_CUDA(cudaMemcpyAsync(hc->dst, hc->src, hc->bytes, cudaMemcpyDeviceToHost, s));
+    if (hc)
+        for (int i = 0; i < hc->n; i++)
+            if (hc->bytes[i])
+                MP_CUDA(cudaMemcpyAsync(hc->dst[i], hc->src[i], hc->bytes[i],
+                                        cudaMemcpyDeviceToHost, s));
     MP_CUDA(cudaMemcpyAsync(g_fctx.red_h, T > 1 ? red : stats,
                             sizeof(int64_t) * (T > 1 ? ST_N + 2 : ST_N), cudaMemcpyDeviceToHost,
                             s));

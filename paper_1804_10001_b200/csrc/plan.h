@@ -11,9 +11,10 @@ namespace mp {
 // before its one synchronisation (host-array callers: one round trip
 // instead of two).  `done` is set when the copy was made.
 struct HostCopy {
-    void *dst;
-    const void *src;
-    size_t bytes;
+    void *dst[2];
+    const void *src[2];
+    size_t bytes[2];
+    int n;
     bool done;
 };
 
