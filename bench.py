@@ -459,7 +459,8 @@ def config_suite(cpu_procs: int, sweep_1e6: bool) -> dict:
     sweep = [("uniform_1e5_s0", "uniform_rr", 100000), ("cnn_1e5_s0", "cnn", 100000),
              ("walk_1e5_s0", "walk", 100000)]
     if sweep_1e6:
-        sweep += [("uniform_1e6_s0", "uniform_rr", 1000000), ("cnn_1e6_s0", "cnn", 1000000)]
+        sweep += [("uniform_1e6_s0", "uniform_rr", 1000000), ("cnn_1e6_s0", "cnn", 1000000),
+                  ("walk_1e6_s0", "walk", 1000000)]
     for key, fam, n in sweep:
         a, f, s = gen_trace(fam, n, 0)
         g = gold.get(key)

@@ -7,7 +7,7 @@ committed and nothing on the GPU box reads /root/reference.
     python tests/golden/make_huge_golden.py [--jobs 7] [--only name,...]
 
 For each configuration of SURVEY.md §8(d) item 5 (uniform / cnn / walk at
-10^5, uniform / cnn at 10^6) and BASELINE.json config 4 (all 4096 LSTM
+10^5, uniform / cnn / walk at 10^6) and BASELINE.json config 4 (all 4096 LSTM
 profiles at L=6 and L=64) it records what the reference's
 `solve_bestfit` (bestfit.py:276-309) returns, as
 

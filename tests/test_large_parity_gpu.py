@@ -15,7 +15,7 @@ from conftest import family_instance, lstm_instances, sha64
 pytestmark = pytest.mark.gpu
 
 SINGLE = ["uniform_1e5_s0", "cnn_1e5_s0", "walk_1e5_s0", "uniform_1e5_s1", "walk_1e5_s1",
-          "uniform_1e6_s0", "cnn_1e6_s0"]
+          "uniform_1e6_s0", "cnn_1e6_s0", "walk_1e6_s0"]
 
 
 @pytest.mark.parametrize("name", SINGLE)
