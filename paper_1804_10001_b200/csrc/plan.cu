@@ -88,6 +88,14 @@ template <int TIER, bool LEAN>
 constexpr int kGroupsPerRound = LEAN ? 2 : (TIER == TIER_SKEL ? 4 : 3);
 template <bool LEAN> constexpr int kSegsPerLane = LEAN ? 1 : 2;
 constexpr int64_t kScanMaxBlocks = 4096;
+// Lifetime samples for the pruning bound: every kLtStep-th priority rank's
+// lifetime in shared memory.  Lifetimes are non-increasing along priority
+// rank (lifetime-major key), so the sample at or after rank e is a LOWER
+// bound on e's lifetime — a slightly weaker but memory-round-free bound.
+constexpr int kLtShift = 7, kLtStep = 1 << kLtShift;
+__host__ __device__ inline size_t lt_bytes(int64_t n) {
+    return ((size_t)(n + kLtStep - 1) / kLtStep + 1) * 4u + 15u & ~size_t(15);
+}
 
 struct PlanArgs {
     const int64_t *trace_ptr;
@@ -183,6 +191,8 @@ struct Win {
     // the shared memory of the cluster's worker CTAs (ranks 1..), read
     // through DSMEM; placed entries are tracked in a per-chunk bitmap in the
     // planner CTA's own shared memory (the remote table stays read-only)
+    const uint32_t *lts; // lifetime samples: lts[k] = lifetime of priority rank
+                         // min(kLtStep k, n - 1), shared memory (pruning bound)
     uint32_t tab;        // shared::cta offset of each worker's slice
     int cshift, pshift;  // chunks / priorities per worker: 1 << shift
     uint32_t *dead;      // per chunk: bit p = position 32 j + p placed
@@ -543,7 +553,7 @@ __device__ __forceinline__ uint32_t query_scan(const Win &w, const uint4 *rec4, 
     return wb;
 }
 
-template <bool STATS, int NW, int TIER, bool LEAN, bool CLU = false>
+template <bool STATS, int NW, int TIER, bool LEAN, bool CLU = false, bool LTS = true>
 __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4, const uint2 *raw2,
                                                  uint32_t *pend, int c0, int c1, uint32_t chi,
                                                  uint32_t clop, uint32_t chip, uint32_t rawhi,
@@ -655,6 +665,8 @@ __device__ __forceinline__ uint32_t query_window(const Win &w, const uint4 *rec4
                 e_used = e;
                 if (CLU) {
                     lstar = dsm_lifetime(w, e);
+                } else if (LTS) {
+                    lstar = w.lts[(e >> kLtShift) + 1];  // lower bound, no memory round
                 } else {
                     const uint2 er = rec_smem ? raw2[e] : ldg_hint(raw2 + e, w.stream);
                     lstar = er.y - er.x;
@@ -765,6 +777,19 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
     uint32_t *pend = reinterpret_cast<uint32_t *>(smem + off) + warp * 2 * kPendCap;
     off += (size_t)NW * 2 * kPendCap * sizeof(uint32_t);
     Win win;
+    if (TIER != TIER_SCAN) {
+        uint32_t *lts = reinterpret_cast<uint32_t *>(smem + off);
+        off += lt_bytes(n);
+        if (prune) {
+            const uint2 *rw2 = a.raw2 + base;
+            const int ns = (n + kLtStep - 1) / kLtStep;
+            for (int k = threadIdx.x; k <= ns; k += 32 * NW) {
+                const uint2 v = rw2[min(k * kLtStep, n - 1)];
+                lts[k] = v.y - v.x;
+            }
+        }
+        win.lts = lts;
+    }
     win.cnt = a.cnt + cb;
     win.keep = l2_policy_keep();
     win.stream = l2_policy_stream();
@@ -1526,7 +1551,7 @@ Layout choose_layout(int64_t nmax, int lcap, size_t hbytes, size_t lim, int nwar
     const size_t skel_b = (size_t)nch * 32 + a16((size_t)nch * 8);
     const size_t tab_b = (size_t)nch * 32 * 8;
     const size_t rec_b = (size_t)nmax * 40;  // records + raw alloc/free
-    size_t used = pend_b;
+    size_t used = pend_b + lt_bytes(nmax);
     if (!force_global) {
         if (!lines_global && used + lines_b <= lim) { l.lines_smem = true; used += lines_b; }
         if (max_tier >= TIER_GROUP && used + grp_b <= lim) {
