@@ -84,8 +84,14 @@ enum { TIER_GLOBAL = 0, TIER_GROUP = 1, TIER_SKEL = 2, TIER_ALL = 3, TIER_SCAN =
 // capped at 128 registers): 2 groups, 1 segment — the smallest memory-level
 // parallelism that compiles without spills at 128 registers, which is what
 // lets 16 traces share an SM (4 warps per SM sub-partition).
+#ifndef MEMPLAN_KG_LEAN
+#define MEMPLAN_KG_LEAN 2
+#endif
+#ifndef MEMPLAN_KG_SKEL
+#define MEMPLAN_KG_SKEL 4
+#endif
 template <int TIER, bool LEAN>
-constexpr int kGroupsPerRound = LEAN ? 2 : (TIER == TIER_SKEL ? 4 : 3);
+constexpr int kGroupsPerRound = LEAN ? MEMPLAN_KG_LEAN : (TIER == TIER_SKEL ? MEMPLAN_KG_SKEL : 3);
 template <bool LEAN> constexpr int kSegsPerLane = LEAN ? 1 : 2;
 constexpr int64_t kScanMaxBlocks = 4096;
 // Lifetime samples for the pruning bound: every kLtStep-th priority rank's
