@@ -147,3 +147,12 @@ def solve_bestfit_batched(instances: Sequence[DsaInstance], *, device: int = 0) 
         plans.append(Plan(offsets=dict(zip(range(1, n + 1), seg)), peak=int(peaks[t]),
                           provenance=Provenance.BESTFIT))
     return plans
+
+
+# host-side skyline inspection types (the reference's bestfit.py debug
+# surface); the planner above never uses them
+def __getattr__(name):
+    if name in ("OffsetLine", "OffsetLineSet", "find_block", "_RemainingBlocks"):
+        from . import skyline
+        return getattr(skyline, name)
+    raise AttributeError(name)

@@ -2,10 +2,9 @@
 copied next to the reference install by baseline/install_ref.sh) imports
 `memplan`; this package answers with paper_1804_10001_b200, the drop-in.
 
-Names of the reference's out-of-scope subsystems (the exact
-branch-and-bound solver, the host-side skyline debug types) are stubs that
-SKIP the calling test, so the run reports them explicitly instead of
-failing collection.  Used only by tests/test_reference_suite_gpu.py."""
+Names of the reference's out-of-scope subsystem (the exact
+branch-and-bound solver) are stubs that SKIP the calling test, so the run
+reports them explicitly instead of failing collection.  Used only by tests/test_reference_suite_gpu.py."""
 
 from paper_1804_10001_b200 import *  # noqa: F401,F403
 from paper_1804_10001_b200 import __all__ as _ours  # noqa: F401
@@ -36,14 +35,5 @@ class _OutOfScopeType(metaclass=_SkipOnUse):
         _pytest.skip(f"{self._name}: out of scope for the B200 build (DESIGN.md §7)")
 
 
-class OffsetLineSet(_OutOfScopeType):
-    _name = "OffsetLineSet (host skyline debug type)"
-
-
-class OffsetLine(_OutOfScopeType):
-    _name = "OffsetLine (host skyline debug type)"
-
-
-find_block = _out_of_scope("find_block (host skyline debug helper)")
 solve_exact = _out_of_scope("solve_exact (exact branch-and-bound solver)")
 brute_force_peak = _out_of_scope("brute_force_peak (exact solver oracle)")

@@ -238,3 +238,41 @@ def test_pool_peak_matches_reference(small_plans):
     assert mp.simulate_pool(events).peak == by["cnn20_seed42"]["pool_peak"] == 704864
     from paper_1804_10001_b200.arena import simulate_pool_peak
     assert simulate_pool_peak(events) == 704864
+
+
+def test_host_skyline_types_drive_equals_oracle():
+    """The host skyline types (skyline.py: OffsetLineSet, find_block,
+    _RemainingBlocks — the reference's step-by-step surface) driven one
+    operation at a time reproduce the oracle's plans (the reference's
+    test_skyline_tracks_placed_blocks_and_solver_agrees, on CPU)."""
+    import random
+
+    import oracle
+    import paper_1804_10001_b200 as mp
+    from paper_1804_10001_b200.skyline import _RemainingBlocks
+    rng = random.Random(17)
+    for _ in range(60):
+        n = rng.randint(1, 40)
+        blocks = []
+        for _ in range(n):
+            a = rng.randint(0, 49)
+            blocks.append((rng.randint(1, 16), a, rng.randint(a + 1, 50)))
+        inst = mp.build_instance(blocks)
+        t_lo = min(b.alloc_time for b in inst.blocks)
+        t_hi = max(b.free_time for b in inst.blocks)
+        ls = mp.OffsetLineSet(t_lo, t_hi)
+        remaining = _RemainingBlocks(inst.blocks)
+        offsets = {}
+        while len(remaining):
+            line = ls.choose_offset()
+            block = remaining.take_best(line.time_lo, line.time_hi)
+            if block is None:
+                ls.lift_up(line)
+            else:
+                offsets[block.id] = ls.place(line, block)
+            tiles = ls.as_tuples()
+            assert tiles[0][0] == t_lo and tiles[-1][1] == t_hi
+            assert all(x[1] == y[0] and x[2] != y[2] for x, y in zip(tiles, tiles[1:]))
+        a, f, s = inst.arrays()
+        ref, _ = oracle.solve_bestfit(a, f, s)
+        assert [offsets[i + 1] for i in range(len(a))] == ref.tolist()

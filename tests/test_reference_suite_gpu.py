@@ -5,9 +5,10 @@ through the import alias tests/refsuite/memplan.
 The test files travel with the reference install (baseline/install_ref.sh
 copies them to baseline/_ref/reftests; git-ignored, shipped to the GPU box).
 Out of scope and not collected: test_cli.py, test_exact.py, test_svg.py
-(CLI, exact solver, SVG — DESIGN.md §7).  Tests that construct the host
-skyline debug types or call the exact solver are SKIPPED by the alias's
-stubs; everything else must pass."""
+(CLI, exact solver, SVG — DESIGN.md §7).  Tests that call the exact solver
+are SKIPPED by the alias's stubs; everything else — including the
+step-by-step skyline tests against the host types in skyline.py — must
+pass."""
 import os
 import re
 import subprocess
@@ -20,8 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REFTESTS = os.path.join(ROOT, "baseline", "_ref", "reftests")
 OUT_OF_SCOPE = ("test_cli.py", "test_exact.py", "test_svg.py")
 # the stubs' skip reasons: the only skips allowed
-ALLOWED_SKIPS = ("OffsetLineSet", "OffsetLine", "find_block", "_RemainingBlocks", "solve_exact",
-                 "brute_force_peak")
+ALLOWED_SKIPS = ("solve_exact", "brute_force_peak")
 
 
 def test_reference_suite_passes_against_the_dropin(tmp_path):
