@@ -1673,8 +1673,10 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     // CTA shape by size: one warp (the planner's own) for tiny traces, so the
     // register-heavy step loop does not cap residency; 256 threads for K0's
     // block sorts beyond that
-    const int variant = nmax <= 128 ? 0 : (nmax <= 512 ? 1 : 2);
+    // (one-warp CTAs up to 256 blocks: LSTM L=64 profiles have 129)
+    const int variant = nmax <= 128 ? 0 : (nmax <= 256 ? 3 : (nmax <= 512 ? 1 : 2));
     const size_t prep_smem = variant == 0 ? sizeof(SmallPrep<32, 8>::Shared)
+                           : variant == 3 ? sizeof(SmallPrep<32, 16>::Shared)
                            : variant == 1 ? sizeof(SmallPrep<128, 8>::Shared)
                                           : sizeof(SmallPrep<256, 16>::Shared);
     // planner layout (TIER_SCAN), sized for 64-bit heights so either fits
@@ -1734,6 +1736,7 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     const int64_t launches0 = g_launches;
     cudaEventRecord(k0, s);
     int rc = variant == 0 ? launch_fused<32, 8>(a, in, (int)T, smem, stats_on, tiny, s)
+           : variant == 3 ? launch_fused<32, 16>(a, in, (int)T, smem, stats_on, tiny, s)
            : variant == 1 ? launch_fused<128, 8>(a, in, (int)T, smem, stats_on, tiny, s)
                           : launch_fused<256, 16>(a, in, (int)T, smem, stats_on, tiny, s);
     if (rc != MP_OK) return rc;
