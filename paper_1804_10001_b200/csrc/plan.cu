@@ -1268,8 +1268,8 @@ template <bool STATS>
 __global__ void __launch_bounds__(32) k_tiny(PlanArgs a, const uint2 *ent, int packed) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int t = a.tlist ? a.tlist[blockIdx.x] : (int)blockIdx.x;
-    if (packed) plan_tiny<true, STATS>(a, ent, t, smem);
-    else plan_tiny<false, STATS>(a, ent, t, smem);
+    if (packed) plan_tiny<true, STATS, !STATS>(a, ent, t, smem);
+    else plan_tiny<false, STATS, !STATS>(a, ent, t, smem);
 }
 
 template <typename HT, bool LINES_SMEM, bool STATS, int NW, int TIER, bool TIMING>

@@ -70,3 +70,25 @@ def test_fuzz_batches(mix):
     for t, (a, f, s) in enumerate(cols):
         ooff, opk = oracle.solve_bestfit(a, f, s)
         assert pks[t] == opk and np.array_equal(off[tp[t]:tp[t + 1]], ooff), (mix, t, len(a))
+
+
+def test_fuzz_tiny_tall_heights():
+    """Single traces on k_tiny whose heights pass 2^27 units (unpacked
+    choose keys: heights relative to the last chosen one, with the
+    saturated fallback when the lowest line jumps by >= 2^27) and windows
+    long enough for the block-summary query."""
+    from paper_1804_10001_b200.bestfit import plan_info, solve_bestfit_arrays
+    rng = np.random.default_rng(77)
+    tiny = 0
+    for trial in range(40):
+        n = int(rng.choice([40, 300, 1500, 4000]))
+        a, f, _ = _trace(rng, n, KINDS[trial % len(KINDS)] if trial % 5 != 3 else "uniform")
+        s = rng.integers(1, 100, n)
+        tall = rng.choice(n, size=min(n, 12), replace=False)
+        s[tall] = (1 << 28) + rng.integers(0, 1 << 20, len(tall))
+        s = s.astype(np.int64)
+        off, pk = solve_bestfit_arrays(a, f, s)
+        tiny += bool(plan_info()["engine"] & 512)  # TIER_TINY ran
+        ooff, opk = oracle.solve_bestfit(a, f, s)
+        assert pk == opk and np.array_equal(off, ooff), (trial, n)
+    assert tiny >= 20, tiny
