@@ -1311,8 +1311,10 @@ __global__ void __launch_bounds__(THREADS, THREADS == 32 ? 16 : 1) k_fused_small
     if (n == 0 || in.total_units[t] < (uint64_t(1) << 32)) {
         int st = PS_LINES_OVERFLOW;
         if constexpr (TINY > 0) {
-            st = in.total_units[t] < (uint64_t(1) << 27) ? plan_tiny<true, STATS>(a, in.ent, t, smem)
-                                                         : plan_tiny<false, STATS>(a, in.ent, t, smem);
+            // block summaries where windows get long (traces > 512 blocks)
+            constexpr bool SUM = THREADS == 256 && !STATS;
+            st = in.total_units[t] < (uint64_t(1) << 27) ? plan_tiny<true, STATS, SUM>(a, in.ent, t, smem)
+                                                         : plan_tiny<false, STATS, SUM>(a, in.ent, t, smem);
             __syncwarp();
         }
         if (st == PS_LINES_OVERFLOW) plan_trace<uint32_t, true, STATS, 1, TIER_SCAN, false, true>(a, t);
@@ -1321,7 +1323,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 32 ? 16 : 1) k_fused_small
     }
 }
 
-constexpr int64_t kFusedMaxBlocks = 2048;
+constexpr int64_t kFusedMaxBlocks = 4096;
 
 // Per-trace stats rows -> one row, on the device, so a batch of thousands of
 // small traces returns 8 * (ST_N + 2) bytes instead of 8 * ST_N per trace.
@@ -1674,13 +1676,18 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     // register-heavy step loop does not cap residency; 256 threads for K0's
     // block sorts beyond that
     // (one-warp CTAs up to 256 blocks: LSTM L=64 profiles have 129)
-    const int variant = nmax <= 128 ? 0 : (nmax <= 256 ? 3 : (nmax <= 512 ? 1 : 2));
+    const int variant = nmax <= 128 ? 0 : nmax <= 256 ? 3 : nmax <= 512 ? 1 : nmax <= 2048 ? 2 : 4;
     const size_t prep_smem = variant == 0 ? sizeof(SmallPrep<32, 8>::Shared)
                            : variant == 3 ? sizeof(SmallPrep<32, 16>::Shared)
                            : variant == 1 ? sizeof(SmallPrep<128, 8>::Shared)
-                                          : sizeof(SmallPrep<256, 16>::Shared);
+                           : variant == 2 ? sizeof(SmallPrep<256, 16>::Shared)
+                                          : sizeof(SmallPrep<256, 32>::Shared);
     // planner layout (TIER_SCAN), sized for 64-bit heights so either fits
     const int sms = sm_count(device);
+    // 2049-4096 blocks: one 256-thread CTA per SM (a 4096-key block sort in
+    // shared memory) — single traces and small batches only; bigger batches
+    // keep the 16-traces-per-SM batched kernel
+    if (variant == 4 && T > sms) return kFusedFallback;
     const size_t lim = smem_limit(device) - 8192;  // two StepShared blocks + prep statics
     const int conc = (int)std::min<int64_t>((T + sms - 1) / sms, 8);
     const size_t budget = conc > 1 ? std::min(lim, (size_t)(228 * 1024) / conc - 8192) : lim;
@@ -1738,7 +1745,8 @@ int plan_fused(const int64_t *trace_ptr_d, int64_t T, int64_t N, int64_t nmax,
     int rc = variant == 0 ? launch_fused<32, 8>(a, in, (int)T, smem, stats_on, tiny, s)
            : variant == 3 ? launch_fused<32, 16>(a, in, (int)T, smem, stats_on, tiny, s)
            : variant == 1 ? launch_fused<128, 8>(a, in, (int)T, smem, stats_on, tiny, s)
-                          : launch_fused<256, 16>(a, in, (int)T, smem, stats_on, tiny, s);
+           : variant == 2 ? launch_fused<256, 16>(a, in, (int)T, smem, stats_on, tiny, s)
+                          : launch_fused<256, 32>(a, in, (int)T, smem, stats_on, tiny, s);
     if (rc != MP_OK) return rc;
     cudaEventRecord(k1, s);
     // one trace: its stats row is the reduction (no extra launch)

@@ -217,10 +217,11 @@ def _check_batch(cols):
     return info
 
 
-@pytest.mark.parametrize("lo,hi", [(0, 128), (100, 512), (400, 2048)])
+@pytest.mark.parametrize("lo,hi", [(0, 128), (100, 512), (400, 2048), (2049, 4096)])
 def test_fused_small_trace_path(lo, hi):
-    """Traces of <= 2048 blocks run K0 + planner in one CTA per trace (one-warp
-    CTAs up to 128 blocks, 4 / 8 warps beyond); more traces than SMs."""
+    """Traces of <= 4096 blocks run K0 + planner in one CTA per trace (one-warp
+    CTAs up to 256 blocks, 4 / 8 warps beyond; 2049-4096 blocks only while
+    the batch has no more traces than SMs)."""
     from paper_1804_10001_b200.workloads import uniform_arrays
     rng = np.random.default_rng(lo)
     cols = []
