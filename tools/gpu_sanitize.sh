@@ -1,6 +1,7 @@
 # compute-sanitizer memcheck / racecheck / synccheck on the planner, validator
 # and prep kernels over small traces (single and batched): TIER_TINY (single
-# and fused, incl. the staircase restart), the LEAN batched kernel, and the
+# and fused — one-warp 128 / 256-block, 4 / 8-warp, 4096-block — incl. the
+# staircase restart; k_tiny with block summaries), the LEAN batched kernel, and the
 # cluster tier (DSMEM table, bulk-copy fills).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
@@ -27,7 +28,7 @@ def batch(sizes, seed):
     tp = np.zeros(len(cols) + 1, np.int64); np.cumsum([len(c[0]) for c in cols], out=tp[1:])
     return tp, [np.concatenate([c[j] for c in cols]) for j in range(3)]
 # fused path: one-warp (<= 128 blocks) and 4-warp CTAs, more traces than SMs
-for sizes in ([13] * 300, [400] * 200):
+for sizes in ([13] * 300, [200] * 300, [400] * 200, [3500] * 8):
     tp, cat = batch(sizes, 7)
     solve_bestfit_batched_arrays(tp, *cat)
 # register-capped LEAN batched kernel + composite / raw-rank K0 (N >= 2^16)
@@ -42,6 +43,11 @@ assert plan_info()["engine"] & 1024, plan_info()
 del os.environ["MEMPLAN_CLUSTER"]
 off3, pk3 = solve_bestfit_arrays(a2, f2, s2)
 assert pk2 == pk3 and (off2 == off3).all()
+# k_tiny after the global K0 (block summaries for long windows)
+os.environ["MEMPLAN_NO_FUSED"] = "1"
+off4, pk4 = solve_bestfit_arrays(a, f, s)
+assert pk4 == pk and (off4 == off).all()
+del os.environ["MEMPLAN_NO_FUSED"]
 print("case ok", pk, pk2)
 PY
 for tool in memcheck racecheck synccheck; do
