@@ -98,6 +98,21 @@ int mp_plan_bestfit_batched(const int64_t *trace_ptr, const int64_t *alloc,
 
 int mp_plan_last_info(mp_plan_info *out);
 
+/* Pipelined batched planning from host arrays: a stream of batches (the
+ * same calls as mp_plan_bestfit_batched, i.e. many independent
+ * solve_bestfit calls, bestfit.py:276) where batch k's upload overlaps
+ * batch k-1's planning and its download overlaps batch k+1's.  Results are
+ * those of mp_plan_bestfit_batched; host arrays must stay untouched until
+ * mp_pipe_wait(ticket) returns.  No reference counterpart (the reference
+ * plans one profile per call); the facade's PlanPipe wraps it. */
+typedef struct mp_plan_pipe mp_plan_pipe;
+mp_plan_pipe *mp_pipe_create(int device);
+int mp_pipe_submit(mp_plan_pipe *pipe, const int64_t *trace_ptr, const int64_t *alloc,
+                   const int64_t *free_, const int64_t *size, int64_t T,
+                   int64_t *offsets_out, int64_t *peaks_out, int flags, int64_t *ticket_out);
+int mp_pipe_wait(mp_plan_pipe *pipe, int64_t ticket);
+void mp_pipe_destroy(mp_plan_pipe *pipe);
+
 /* ---- validation: replaces verify_plan(instance, plan) (verifier.py:44-81)
  * over colliding_pairs (core.py:227-249).  The report carries the exact
  * 128-bit sum of size*lifetime so the facade can compute utilisation

@@ -93,6 +93,11 @@ SIGNATURES = [
     ("mp_plan_bestfit_batched", ctypes.c_int, [VP, VP, VP, VP, ctypes.c_int64, VP, VP,
                                                ctypes.c_int, ctypes.c_int, VP]),
     ("mp_plan_last_info", ctypes.c_int, [ctypes.POINTER(PlanInfo)]),
+    ("mp_pipe_create", VP, [ctypes.c_int]),
+    ("mp_pipe_submit", ctypes.c_int, [VP, VP, VP, VP, VP, ctypes.c_int64, VP, VP, ctypes.c_int,
+                                      P64]),
+    ("mp_pipe_wait", ctypes.c_int, [VP, ctypes.c_int64]),
+    ("mp_pipe_destroy", None, [VP]),
     ("mp_verify", ctypes.c_int, [VP, VP, VP, VP, ctypes.c_int64, ctypes.POINTER(VerifyReportC),
                                  VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int, VP]),
     ("mp_clique_lower_bound", ctypes.c_int, [VP, VP, VP, ctypes.c_int64, P64, ctypes.c_int,

@@ -131,6 +131,63 @@ def solve_bestfit_batched_arrays(trace_ptr, alloc, free, size, *, device: int = 
     return off, peaks
 
 
+class PlanPipe:
+    """Pipelined batched planning from host arrays (`mp_pipe_*`): while the
+    GPU plans batch k, batch k+1 uploads and batch k-1 downloads.  Each
+    `submit` returns a ticket; `wait(ticket)` returns that batch's
+    (offsets, peaks), equal to `solve_bestfit_batched_arrays` on the same
+    inputs.  Inputs are kept referenced until their ticket is waited for;
+    page-locked arrays (torch `pin_memory`) let the copies run
+    asynchronously.  At most two batches are in flight: a third submit
+    waits for the first one's results."""
+
+    def __init__(self, device: int = 0):
+        self._lib = N.lib()
+        self._p = self._lib.mp_pipe_create(device)
+        if not self._p:
+            check(N.MP_ERR_NO_DEVICE)
+        self._live = {}
+
+    def submit(self, trace_ptr, alloc, free, size, *, offsets_out=None, peaks_out=None,
+               flags: int = 0) -> int:
+        tp = N.as_i64(trace_ptr)
+        a, f, s = N.as_i64(alloc), N.as_i64(free), N.as_i64(size)
+        T = len(tp) - 1
+        off = np.empty(len(a), dtype=np.int64) if offsets_out is None else offsets_out
+        pk = np.zeros(max(T, 0), dtype=np.int64) if peaks_out is None else peaks_out
+        ticket = ctypes.c_int64(-1)
+        rc = self._lib.mp_pipe_submit(self._p, N.ptr(tp), N.ptr(a), N.ptr(f), N.ptr(s), T,
+                                      N.ptr(off), N.ptr(pk), flags, ctypes.byref(ticket))
+        if ticket.value >= 0:
+            self._live[ticket.value] = (tp, a, f, s, off, pk)
+        check(rc)
+        return ticket.value
+
+    def wait(self, ticket: int):
+        rc = self._lib.mp_pipe_wait(self._p, ticket)
+        bufs = self._live.pop(ticket, None)
+        check(rc)
+        return bufs[4], bufs[5]
+
+    def close(self) -> None:
+        if self._p:
+            self._lib.mp_pipe_destroy(self._p)
+            self._p = None
+            self._live.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def solve_bestfit_batched(instances: Sequence[DsaInstance], *, device: int = 0) -> list[Plan]:
     """Plan many independent instances in one batched launch."""
     cols = [inst.arrays() for inst in instances]
