@@ -103,7 +103,9 @@ int mp_plan_last_info(mp_plan_info *out);
  * solve_bestfit calls, bestfit.py:276) where batch k's upload overlaps
  * batch k-1's planning and its download overlaps batch k+1's.  Results are
  * those of mp_plan_bestfit_batched; host arrays must stay untouched until
- * mp_pipe_wait(ticket) returns.  No reference counterpart (the reference
+ * mp_pipe_wait(ticket) returns.  At most two batches are in flight (a third
+ * submit waits for the first); a ticket's status stays available for 1024
+ * further submits.  No reference counterpart (the reference
  * plans one profile per call); the facade's PlanPipe wraps it. */
 typedef struct mp_plan_pipe mp_plan_pipe;
 mp_plan_pipe *mp_pipe_create(int device);

@@ -63,11 +63,16 @@ struct mp_plan_pipe {
     std::map<int64_t, std::string> err;
     int64_t next = 0;
     int64_t limit = 0;  // blocks one slot / one K0 pass takes (pipe_block_limit)
+    int64_t expired = 0;  // tickets below this were forgotten (kExpire behind `next`)
     bool stop = false;
     std::thread worker;
 };
 
 namespace {
+
+// results of the last kExpire tickets are kept for mp_pipe_wait (older
+// ones were synced when their slot was reused)
+constexpr int64_t kExpire = 1024;
 
 int64_t pipe_block_limit() {
     if (const char *env = getenv("MEMPLAN_MAX_BATCH_BLOCKS")) return std::max<int64_t>(1, atoll(env));
@@ -204,6 +209,13 @@ int mp_pipe_submit(mp_plan_pipe *p, const int64_t *trace_ptr, const int64_t *all
     j.direct = j.N <= p->limit;
     j.ticket = p->next++;
     j.slot = (int)(j.ticket & 1);
+    while (!p->result.empty() && p->result.begin()->first < j.ticket - kExpire) {
+        const int64_t old = p->result.begin()->first;
+        p->result.erase(old);
+        p->synced.erase(old);
+        p->err.erase(old);
+        p->expired = old + 1;
+    }
     *ticket_out = j.ticket;
     Slot &sl = p->slot[j.slot];
     // the slot's previous batch must have landed on the host
@@ -252,6 +264,10 @@ int mp_pipe_wait(mp_plan_pipe *p, int64_t ticket) {
     std::unique_lock<std::mutex> lk(p->mu);
     if (ticket < 0 || ticket >= p->next) {
         set_error("unknown pipe ticket");
+        return MP_ERR_INVALID;
+    }
+    if (ticket < p->expired) {
+        set_error("pipe ticket expired (more than 1024 submits ago)");
         return MP_ERR_INVALID;
     }
     const int rc = finish(p, lk, ticket);
