@@ -98,3 +98,20 @@ def test_pipe_rejects_bad_batch_and_keeps_going():
             pipe.submit(bad, a, f, s)
         off, pk = pipe.wait(pipe.submit(tp, a, f, s))
         assert np.array_equal(off, wo) and np.array_equal(pk, wp)
+
+
+def test_pipe_tickets_expire():
+    from paper_1804_10001_b200.bestfit import PlanPipe
+    tp = np.array([0, 3], np.int64)
+    a, f, s = np.array([0, 1, 2]), np.array([2, 3, 4]), np.array([512, 512, 1024])
+    with PlanPipe() as pipe:
+        first = pipe.submit(tp, a, f, s)
+        off0, pk0 = pipe.wait(first)
+        for _ in range(1030):
+            t = pipe.submit(tp, a, f, s)
+            off, pk = pipe.wait(t)
+            assert np.array_equal(off, off0) and np.array_equal(pk, pk0)
+        with pytest.raises(ValueError):
+            pipe.wait(first)
+        with pytest.raises(ValueError):
+            pipe.wait(t + 5)
