@@ -884,6 +884,7 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
     bool known = true;
     int c = 0;
     K ck = KO::make(0, 0);
+    HT hbase = 0;  // the last chosen height (a lower bound of every line's)
     HT hP = 0, hN = 0;
     bool hasP = false, hasN = false;
     uint32_t clop = 0, chip = 0, chi = 0, craw = 0, rawhi = 0;
@@ -908,6 +909,26 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
                         const HT hmin = KO::warp_min_h(KO::h(k));
                         c = __ffs(__ballot_sync(kFull, KO::h(k) == hmin && lane < nl)) - 1;
                         ck = KO::make(hmin, __shfl_sync(kFull, KO::lo(k), c));
+                    } else if (sizeof(HT) == 4 && nl <= 128 && [&] {
+                        // one reduction over (height relative to the last
+                        // choice, saturated) << 7 | line: the lowest height
+                        // never decreases; a saturated minimum falls back
+                        constexpr uint32_t SAT = (1u << 25) - 1u;
+                        uint32_t pk = 0xFFFFFFFFu;
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int i = lane + 32 * u;
+                            if (i < nl) {
+                                const uint32_t rel = (uint32_t)(KO::h(L[i].key) - hbase);
+                                pk = min(pk, (min(rel, SAT) << 7) | (uint32_t)i);
+                            }
+                        }
+                        const uint32_t km = __reduce_min_sync(kFull, pk);
+                        if ((km >> 7) >= SAT) return false;
+                        c = (int)(km & 127u);
+                        ck = L[c].key;
+                        return true;
+                    }()) {
                     } else if (nl <= 128) {
                         // heights first (one reduction), then the leftmost
                         // line at that height (a second reduction over line
@@ -940,6 +961,7 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
                         c = __shfl_sync(kFull, bi, __ffs(__ballot_sync(kFull, bk == ck)) - 1);
                     }
                 }
+                hbase = KO::h(ck);
                 hasP = c > 0;
                 hasN = c + 1 < nl;
                 const LR ln = L[c + 1];
