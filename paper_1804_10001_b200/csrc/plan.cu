@@ -1122,6 +1122,17 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
             __syncwarp();
             if (mv) L[lane + d] = v;
             __syncwarp();
+        } else if (!LEAN && d != 0 && nl - (c + 1 + e) < 32) {
+            // short tail of a long skyline (most shifts: the chosen line
+            // sits near its end): one line per lane (single-trace kernels;
+            // the register-capped batched loop measured slower with it)
+            const int i = c + 1 + e + lane;
+            const bool mv = i <= nl;
+            LR v;
+            if (mv) v = L[i];
+            __syncwarp();
+            if (mv) L[i + d] = v;
+            __syncwarp();
         } else if (d != 0) {
             const int from = c + 1 + e, to = nl;  // inclusive
             const int nblk = (to - from) >> 7;
