@@ -518,6 +518,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world > 1:
         backend = os.environ.get("MEMPLAN_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # NCCL's init lines (rank count, transport) on stderr, for the record
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
@@ -728,6 +731,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                   "api": "mp_plan_bestfit_batched, median per call",
                                   "results_equal_device_path": e2e_exact}},
             "gpu_launches": launches,
+            "collective": ({"backend": dist.get_backend(), "nranks": dist.get_world_size(),
+                            "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))
+                            if dist.get_backend() == "nccl" else None,
+                            "op": "grouped send/recv gather of offsets and peaks to rank 0 "
+                                  "(paper_1804_10001_b200.dist.gather_device)"}
+                           if world > 1 else None),
             "roofline": roof,
             "cpu_baseline": cpu,
             "clocks": clk,
