@@ -485,6 +485,12 @@ def config_suite(cpu_procs: int, sweep_1e6: bool) -> dict:
     return out
 
 
+def nccl_version():
+    import torch
+    v = torch.cuda.nccl.version()
+    return ".".join(map(str, v)) if isinstance(v, tuple) else str(v)
+
+
 def bench_config(args, world):
     if args.workload == "lstm":
         return {"workload": f"4096 variable-length LSTM seq2seq profiles (L={args.lstm_layers}, "
@@ -732,8 +738,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                   "results_equal_device_path": e2e_exact}},
             "gpu_launches": launches,
             "collective": ({"backend": dist.get_backend(), "nranks": dist.get_world_size(),
-                            "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))
-                            if dist.get_backend() == "nccl" else None,
+                            "nccl_version": nccl_version() if dist.get_backend() == "nccl"
+                            else None,
                             "op": "grouped send/recv gather of offsets and peaks to rank 0 "
                                   "(paper_1804_10001_b200.dist.gather_device)"}
                            if world > 1 else None),
