@@ -527,6 +527,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             # NCCL's init lines (rank count, transport) on stderr, for the record
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout: the JSON line
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
