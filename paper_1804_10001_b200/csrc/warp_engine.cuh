@@ -102,11 +102,8 @@ __device__ __forceinline__ int plan_tiny(const PlanArgs &a, const uint2 *ent, co
     uint32_t sk0 = NONE, sf0 = 0, sk1 = NONE, sf1 = 0;
     unsigned long long dirty = ~0ull;
 
-    while (placed < n) {
-        if (++steps > bound) {  // R8 (bestfit.py:297)
-            status = PS_LOOP_BOUND;
-            break;
-        }
+    while (placed < n && steps < bound) {  // R8 (bestfit.py:297): checked below
+        ++steps;
         // ---- choose (R3): lowest, then leftmost line ----
         int c;
         uint32_t ch;
@@ -249,12 +246,13 @@ __device__ __forceinline__ int plan_tiny(const PlanArgs &a, const uint2 *ent, co
             h2 = ch;
             q2 = qf;
             m = (hasL ? 1 : 0) + (mP ? 0 : 1) + (hasR ? 1 : 0);
+            // only a place can grow the skyline (a lift has d <= 0)
+            if (nl + m - e > 32) {
+                status = PS_LINES_OVERFLOW;
+                break;
+            }
         }
         const int d = m - 1 - e;
-        if (nl + d + 1 > 32) {
-            status = PS_LINES_OVERFLOW;
-            break;
-        }
         // splice: lane i keeps its line (i < c), takes new line i - c
         // (i < c + m), or its old line i - d
         const uint32_t sh = __shfl_sync(full, Lh, (lane - d) & 31);
@@ -269,6 +267,10 @@ __device__ __forceinline__ int plan_tiny(const PlanArgs &a, const uint2 *ent, co
         nl += d;
         maxl = max(maxl, nl);
         __syncwarp();  // the retired entry is visible to the next scan
+    }
+    if (status == PS_OK && placed < n) {  // R8: the bound ran out
+        status = PS_LOOP_BOUND;
+        steps = bound + 1;
     }
     __syncwarp();
     // offsets per block index (id order), one pass: offset = height * unit
