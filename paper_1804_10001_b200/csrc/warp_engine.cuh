@@ -102,7 +102,8 @@ __device__ __forceinline__ int plan_tiny(const PlanArgs &a, const uint2 *ent, co
     uint32_t sk0 = NONE, sf0 = 0, sk1 = NONE, sf1 = 0;
     unsigned long long dirty = ~0ull;
 
-    while (placed < n && steps < bound) {  // R8 (bestfit.py:297): checked below
+    bool illegal = false;
+    while (placed < n && steps < bound && !illegal) {  // R8 (bestfit.py:297): checked below
         ++steps;
         // ---- choose (R3): lowest, then leftmost line ----
         int c;
@@ -210,10 +211,9 @@ __device__ __forceinline__ int plan_tiny(const PlanArgs &a, const uint2 *ent, co
         if (wb == NONE) {
             // lift_up (R5, bestfit.py:180-201)
             ++lifts;
-            if (!hasP && !hasN) {
-                status = PS_ILLEGAL_LIFT;
-                break;
-            }
+            // lifting the only line (bestfit.py:185-186) ends the loop at
+            // its condition; this step's splice is discarded with the plan
+            illegal = !hasP && !hasN;
             const bool intoN = !hasP || (hasN && hP > hN);
             const bool intoP = !intoN && (!hasN || hP < hN);
             e = intoP ? 0 : 1;
@@ -268,7 +268,9 @@ __device__ __forceinline__ int plan_tiny(const PlanArgs &a, const uint2 *ent, co
         maxl = max(maxl, nl);
         __syncwarp();  // the retired entry is visible to the next scan
     }
-    if (status == PS_OK && placed < n) {  // R8: the bound ran out
+    if (illegal) {
+        status = PS_ILLEGAL_LIFT;
+    } else if (status == PS_OK && placed < n) {  // R8: the bound ran out
         status = PS_LOOP_BOUND;
         steps = bound + 1;
     }
