@@ -894,9 +894,10 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
     long long tc = TIMING ? clock64() : 0, tstep = tc;
     for (;;) {
         // ======== leader: choose (R3) ========
-        if (warp == 0) {
+        if (NW == 1 || warp == 0) {
             if (placed >= n || ++steps > bound) {
                 if (placed < n) status = PS_LOOP_BOUND;  // R8
+                if (NW == 1) break;  // one warp: leave right here
                 if (lane == 0) ss.done = 1;
             } else {
                 if (!known) {
@@ -979,7 +980,7 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
             }
         }
         if (NW > 1) __syncthreads();  // [A] choice published
-        if (NW > 1 ? ss.done : (placed >= n || status != PS_OK)) break;
+        if (NW > 1 && ss.done) break;
 
         if (TIMING) { const long long t2 = clock64(); tph[0] += t2 - tc; tc = t2; }
         // ======== all warps: query (R4) ========
@@ -1109,7 +1110,7 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
 
         // ---- apply: shift the tail [c+1+e, nl] (incl. sentinel) by d ----
         const int d = m - 1 - e;
-        if (nl + d > lcap) {
+        if (gbest != kNone && nl + d > lcap) {  // only a place grows the skyline
             status = PS_LINES_OVERFLOW;
             placed = n;
             continue;
