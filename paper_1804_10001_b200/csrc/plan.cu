@@ -1059,11 +1059,10 @@ __device__ __forceinline__ void plan_trace(const PlanArgs &a, const int t) {
         if (gbest == kNone) {
             // lift_up (R5)
             ++lifts;
-            if (!hasP && !hasN) {
+            if (!hasP && !hasN) {  // lifting the only line (bestfit.py:185-186)
                 status = PS_ILLEGAL_LIFT;
-                placed = n;  // leave through the done path next round
-                continue;
-            }
+                placed = n;  // the loop ends at its next top check; this
+            }                // step's harmless splice is discarded with the plan
             const bool intoN = !hasP || (hasN && hP > hN);
             const bool intoP = !intoN && (!hasN || hP < hN);
             e = intoP ? 0 : 1;
